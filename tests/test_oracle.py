@@ -1,0 +1,339 @@
+"""Pins of the CPU oracle O1 (oracle/dg_oracle.c) against things other than
+itself: closed forms, invariants, exact symmetries, a dense brute-force
+assembly derived independently (O2, oracle/dense.py), the paper's printed
+values, and an independent implementation's numbers.
+
+Each test names the plausible mistake it is there to catch.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import dense as O2
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+RNG = np.random.default_rng(20190715)
+
+
+def c1_mask():
+    n = 32
+    c = np.arange(n) + 0.5
+    X, Y = np.meshgrid(c, c)
+    return (((X - 16) ** 2 + (Y - 16) ** 2) <= 64).astype(np.uint8)
+
+
+# ---------------------------------------------------------------- basis / matrices
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_basis_partition_of_unity_and_nodal(orc, p):
+    """Eq. (8) Lagrange basis: sum_j N_j = 1 and N_i(x_j) = delta_ij (catches a
+    wrong node order or a mis-typed barycentric formula)."""
+    ref = orc.reference(p)
+    for t in (0, 1):
+        nodes = ref["nodes"][t]
+        V = orc.basis(p, t, nodes)
+        assert np.allclose(V, np.eye(orc.ndof(p)), atol=1e-14)
+        pts = RNG.random((50, 2))
+        pts = np.where((pts[:, 1] < pts[:, 0])[:, None] == (t == 0), pts, pts[:, ::-1])
+        assert np.allclose(orc.basis(p, t, pts).sum(axis=1), 1.0, atol=1e-13)
+
+
+def test_p1_mass_matrix_closed_form(orc):
+    """P1 M_T = (h^2/24)[[2,1,1],[1,2,1],[1,1,2]] on a triangle of area h^2/2."""
+    h = 0.3
+    ref = orc.reference(1, h)
+    M = h * h / 24 * np.array([[2, 1, 1], [1, 2, 1], [1, 1, 2]])
+    for t in (0, 1):
+        assert np.allclose(ref["M"][t], M, rtol=1e-14, atol=0)
+
+
+@pytest.mark.parametrize("p,expect", [(1, [1 / 6] * 3), (2, [0, 0, 0, 1 / 6, 1 / 6, 1 / 6])])
+def test_mass_weights(orc, p, expect):
+    """int N_j = row sums of M (partition of unity): P1 h^2/6 each; P2 vertex 0,
+    edge h^2/6 (textbook quadratic-triangle weights)."""
+    h = 0.7
+    ref = orc.reference(p, h)
+    for t in (0, 1):
+        assert np.allclose(ref["M"][t].sum(axis=1), h * h * np.array(expect), atol=1e-15)
+        w, _ = np.linalg.eigh(ref["M"][t])
+        assert w.min() > 0                        # SPD
+
+
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_reference_matrices_match_exact_integration(orc, p):
+    """O1's Gauss-quadrature M, Dc, E-, E+ equal O2's exact monomial integrals
+    (catches a too-low quadrature order, a missing 1/h in the gradient, a wrong
+    face length or a wrong neighbour parametrisation)."""
+    h = 0.25
+    ref = orc.reference(p, h)
+    M, Dc, Em, Ep = O2.ref_matrices(p, h)
+    tol = 1e-13 if p < 3 else 1e-11
+    assert np.allclose(ref["M"], M, atol=tol * h * h)
+    assert np.allclose(ref["Dc"], Dc, atol=tol * h)
+    assert np.allclose(ref["Em"], Em, atol=tol * h)
+    assert np.allclose(ref["Ep"], Ep, atol=tol * h)
+
+
+def test_normals_outward_unit(orc):
+    ref = orc.reference(1)
+    n = ref["nrm"]
+    assert np.allclose(np.linalg.norm(n, axis=2), 1.0)
+    # L: bottom, right, diagonal; U: top, left, diagonal
+    assert np.allclose(n[0, 0], [0, -1]) and np.allclose(n[0, 1], [1, 0])
+    assert np.allclose(n[1, 0], [0, 1]) and np.allclose(n[1, 1], [-1, 0])
+    assert np.allclose(n[0, 2], -n[1, 2]) and np.allclose(n[0, 2], np.array([-1, 1]) / np.sqrt(2))
+
+
+# ---------------------------------------------------------------- operator vs dense brute force
+@pytest.mark.parametrize("p", [1, 2, 3])
+@pytest.mark.parametrize("bc", [0, 1])
+def test_apply_L_matches_dense_assembly(orc, p, bc):
+    """O1 element loops == O2 global dense assembly on random <=8x8 masks
+    (SPEC S:252 'oracle equivalence ... to 1e-12'); catches sign, index,
+    transposed-operand and flux-weight mistakes anywhere in Eq. (7)."""
+    rng = np.random.default_rng(p * 10 + bc)
+    d = orc.ndof(p)
+    for trial in range(3):
+        ny, nx = rng.integers(4, 9, size=2)
+        mask = (rng.random((ny, nx)) < 0.35).astype(np.uint8)
+        u = rng.standard_normal((ny, nx, 2, d))
+        u[mask.astype(bool)] = 0.0
+        h, D = 0.5 + rng.random(), 0.5 + 2 * rng.random()
+        ref = (O2.assemble(p, h, D, mask, bc) @ u.reshape(-1)).reshape(u.shape)
+        got = orc.apply_L(p, h, D, mask, u, bc)
+        tol = 1e-12 if p < 3 else 1e-11
+        assert np.linalg.norm(got - ref) <= tol * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_ssprk3_steps_match_dense(orc, p):
+    """Full scheme (Dirac data, SSP-RK3, moments) vs dense stepping."""
+    rng = np.random.default_rng(7 + p)
+    mask = (rng.random((8, 7)) < 0.3).astype(np.uint8)
+    mask[4, 3] = 0
+    dt = (1 / 32) if p == 1 else (1 / 128)
+    mom, dens = orc.solve(p, 1.0, 1.0, mask, [(3, 4)], dt, 40, keep_density=True)
+    u0 = O2.delta(p, 1.0, 7, 8, (3, 4))
+    assert np.allclose(orc.project_delta(p, 1.0, 7, 8, (3, 4)), u0, atol=1e-13)
+    u = O2.ssprk3(O2.assemble(p, 1.0, 1.0, mask), u0, dt, 40).reshape(dens[0].shape)
+    assert np.linalg.norm(dens[0] - u) <= 1e-12 * np.linalg.norm(u)
+    assert np.allclose(mom[0], O2.moments(p, 1.0, u, (3, 4)), rtol=1e-12, atol=1e-13)
+
+
+def test_composite_operator_is_5_point(orc):
+    """After eliminating q, a pixel couples only to its 4 face neighbours
+    (SURVEY F3); the P1 all-open self block is the dyadic table of App. A.11."""
+    blocks, stray = O2.composite_blocks(1, 15)
+    assert stray == 0.0
+    self_row0 = [-53 / 2, 1, -9 / 2, 9 / 2, 9 / 2, 9]
+    assert np.allclose(blocks[(0, 0)][0], self_row0, atol=1e-13)
+    # every row sums to zero across the 5 blocks (constants in the interior)
+    tot = sum(blocks.values())
+    assert np.abs(tot.sum(axis=1)).max() < 1e-12
+
+
+# ---------------------------------------------------------------- invariants
+def test_initial_data_closed_form(orc):
+    """P1 split-delta coefficients are +3/h^2 at the two diagonal vertices and
+    -3/h^2 at the right-angle vertex (1/2 M^-1 N(x_c), by hand)."""
+    h = 0.5
+    u = orc.project_delta(1, h, 3, 3, (1, 1))
+    assert np.allclose(u[1, 1, 0], np.array([3, -3, 3]) / h ** 2, rtol=1e-14)
+    assert np.allclose(u[1, 1, 1], np.array([3, 3, -3]) / h ** 2, rtol=1e-14)
+    assert np.count_nonzero(u) == 6
+
+
+@pytest.mark.parametrize("p,expect", [(1, [[1 / 20, 1 / 10], [1 / 10, 1 / 20]]), (2, [[0, 0], [0, 0]])])
+def test_initial_sigma_closed_form(orc, p, expect):
+    """Sigma(0) of the projected Dirac: P1 h^2[[1/20,1/10],[1/10,1/20]]; P2 0
+    (P2 integrates quadratics exactly, so the projection keeps the Dirac's
+    zero second moments).  Mass 1, mean at the source."""
+    h = 0.5
+    mask = np.zeros((5, 5), np.uint8)
+    mom = orc.solve(p, h, 1.0, mask, [(2, 2)], 0.01, 0)
+    S, mu = orc.sigma(mom)
+    assert abs(mom[0, 0] - 1) < 1e-14
+    assert np.allclose(mu, 0, atol=1e-15)
+    assert np.allclose(S, h * h * np.array(expect), atol=1e-15)
+
+
+def test_mass_conserved_and_axons_static(orc):
+    """REFLECT: total mass exact (P:204 no flow through axon walls; F2) and
+    masked dofs identically zero for all t."""
+    rng = np.random.default_rng(3)
+    mask = (rng.random((20, 20)) < 0.45).astype(np.uint8)
+    free = np.argwhere(mask == 0)
+    src = [tuple(free[k][::-1]) for k in (0, len(free) // 2, len(free) - 1)]
+    mom, dens = orc.solve(1, 1.0, 1.0, mask, src, 1 / 32, 500, keep_density=True)
+    assert np.abs(mom[:, 0] - 1).max() < 1e-12
+    assert np.abs(dens[:, mask.astype(bool)]).max() == 0.0
+
+
+def test_absorbing_boundary_loses_mass(orc):
+    """Eq. (4) u = 0 on the outer square: mass leaves once the density reaches it."""
+    mask = np.zeros((10, 10), np.uint8)
+    m_ref = orc.solve(1, 1.0, 1.0, mask, [(5, 5)], 1 / 32, 300, outer_bc=0)
+    m_abs = orc.solve(1, 1.0, 1.0, mask, [(5, 5)], 1 / 32, 300, outer_bc=1)
+    assert abs(m_ref[0, 0] - 1) < 1e-12
+    assert m_abs[0, 0] < 0.9
+
+
+@pytest.mark.parametrize("h,D", [(1.0, 1.0), (0.5, 2.0)])
+def test_free_space_sigma_p1_closed_form(orc, h, D):
+    """P1 free space: Sigma(Delta) = 2 D Delta I + h^2 [[1/20,1/15],[1/15,1/20]]
+    once the ~0.25 h^2/D transient has passed; sharpens the
+    paper's Sigma = 2Tk I.  Catches a wrong D/h scaling, a
+    missing flux half, a wrong RK weight."""
+    dt = h * h / D / 32
+    nsteps = 64
+    delta = nsteps * dt
+    n = 72
+    mask = np.zeros((n, n), np.uint8)
+    mom = orc.solve(1, h, D, mask, [(36, 36)], dt, nsteps)
+    S, mu = orc.sigma(mom)
+    expect = 2 * D * delta * np.eye(2) + h * h * np.array([[1 / 20, 1 / 15], [1 / 15, 1 / 20]])
+    assert np.allclose(S, expect, rtol=1e-12, atol=1e-13 * expect[0, 0])
+    assert np.allclose(mu, 0, atol=1e-13 * h)
+
+
+def test_free_space_sigma_p2_closed_form(orc):
+    """P2 free space: Sigma(Delta) = 2 D Delta I exactly, also fully discrete
+    (the moment ODE is linear in t, which SSP-RK3 integrates exactly)."""
+    h, D = 1.0, 1.0
+    dt = 1 / 128
+    nsteps = 256
+    n = 104
+    mask = np.zeros((n, n), np.uint8)
+    mom = orc.solve(2, h, D, mask, [(52, 52)], dt, nsteps)
+    S, _ = orc.sigma(mom)
+    assert np.allclose(S, 2 * D * nsteps * dt * np.eye(2), rtol=0, atol=2e-12)
+
+
+def test_paper_analytic_value(orc):
+    """k = 450 um^2/s, T = 0.036 s gives 2Tk = 32.4.  The same
+    physics in grid units (h = 0.125 um) on a smaller free grid: P2 gives
+    exactly 2 D Delta, i.e. 32.4 um^2 at T = 0.036 s."""
+    paper = json.load(open(os.path.join(GOLD, "paper_values.json")))["free_diffusion_analytic"]
+    k, T = paper["k0_um2_per_s"], paper["T_s"]
+    assert abs(2 * T * k - paper["sigma_diag"]) < 1e-12
+    # physical units h = 0.125 um, D = 450 um^2/s, over T' = T/1024 so that a
+    # small grid keeps the walls >= 25 sigma away (P2 tails):
+    # Sigma' = 32.4/1024 um^2 exactly; dt chosen stable (D dt/h^2 <= 0.013).
+    h, scale = 0.125, 1024
+    nsteps = 128
+    dt = (T / scale) / nsteps
+    assert k * dt / h ** 2 < 0.013
+    n = 80
+    mom = orc.solve(2, h, k, np.zeros((n, n), np.uint8), [(40, 40)], dt, nsteps)
+    S, _ = orc.sigma(mom)
+    assert np.allclose(S * scale, np.diag([32.4, 32.4]), rtol=0, atol=1e-10)
+
+
+# ---------------------------------------------------------------- symmetries (F8)
+def _case(seed):
+    rng = np.random.default_rng(seed)
+    mask = (rng.random((18, 18)) < 0.4).astype(np.uint8)
+    free = np.argwhere(mask[5:13, 5:13] == 0) + 5
+    src = [(int(f[1]), int(f[0])) for f in free[:4]]
+    return mask, src
+
+
+def test_transpose_symmetry_exact(orc):
+    """x <-> y swaps L and U of every pixel (the diagonal is its own mirror),
+    so Sigma' = P Sigma P^T exactly (catches an x/y or L/U asymmetry)."""
+    mask, src = _case(11)
+    S, mu = orc.sigma(orc.solve(1, 1.0, 1.0, mask, src, 1 / 32, 96))
+    St, mut = orc.sigma(orc.solve(1, 1.0, 1.0, mask.T.copy(), [(j, i) for i, j in src], 1 / 32, 96))
+    assert np.allclose(St, S[::-1, ::-1], rtol=1e-13, atol=1e-14)
+    assert np.allclose(mut, mu[::-1], atol=1e-14)
+
+
+def test_rotation_180_symmetry_exact(orc):
+    """180 degrees maps the mesh onto itself: Sigma' = Sigma, mu' = -mu."""
+    mask, src = _case(12)
+    n = mask.shape[0]
+    S, mu = orc.sigma(orc.solve(1, 1.0, 1.0, mask, src, 1 / 32, 96))
+    Sr, mur = orc.sigma(orc.solve(1, 1.0, 1.0, mask[::-1, ::-1].copy(),
+                                  [(n - 1 - i, n - 1 - j) for i, j in src], 1 / 32, 96))
+    assert np.allclose(Sr, S, rtol=1e-13, atol=1e-14)
+    assert np.allclose(mur, -mu, atol=1e-14)
+
+
+def test_sigma_symmetric_psd_and_hindered(orc):
+    """Sigma stored symmetric; eigenvalues > 0; walls hinder: Sigma_ii < 2 D Delta
+    (the paper's case study 19.50 < 32.4)."""
+    mask, src = _case(13)
+    S, _ = orc.sigma(orc.solve(1, 1.0, 1.0, mask, src, 1 / 32, 96))
+    assert S[0, 1] == S[1, 0]
+    assert np.linalg.eigvalsh(S).min() > 0
+    assert S[0, 0] < 2 * 3.0 and S[1, 1] < 2 * 3.0
+
+
+# ---------------------------------------------------------------- stability (F5)
+def test_spectral_radius_and_rk3_stability(orc):
+    """rho(L) <= 60 D/h^2 (P1 Bloch bound): SSP-RK3 is stable at
+    0.98 dt_max and blows up at 1.05 dt_max on a free grid."""
+    L = O2.assemble(1, 1.0, 1.0, np.zeros((10, 10), np.uint8))
+    lam = np.linalg.eigvals(L)
+    assert np.abs(lam).max() <= 60.0 + 1e-9
+    assert lam.real.max() < 1e-10
+    rho = 60.0
+    dtmax = 2.5127453 / rho
+    rng = np.random.default_rng(5)
+    mask = np.zeros((24, 24), np.uint8)
+    u0 = rng.standard_normal((24, 24, 2, 3))
+    ok = orc.advance(1, 1.0, 1.0, mask, u0, 0.98 * dtmax, 300)
+    bad = orc.advance(1, 1.0, 1.0, mask, u0, 1.05 * dtmax, 300)
+    assert np.linalg.norm(ok) <= np.linalg.norm(u0)
+    assert np.linalg.norm(bad) > 1e6 * np.linalg.norm(u0)
+
+
+# ---------------------------------------------------------------- independent implementation
+def test_config1_matches_independent_implementation(orc):
+    """SURVEY App. A.10 (independent scratch implementation) config-1 values."""
+    g = json.load(open(os.path.join(GOLD, "c1_independent_A10.json")))
+    tol = g["tolerance_rel"]
+    mask = c1_mask()
+    assert mask.sum() == 208
+    m1 = orc.solve(1, 1.0, 1.0, mask, [(4, 16)], 1 / 32, 1)[0]
+    assert np.allclose(m1[[0, 3, 4, 5]], np.array(g["reflect_1"]["m"])[[0, 3, 4, 5]], rtol=tol)
+    mom, dens = orc.solve(1, 1.0, 1.0, mask, [(4, 16)], 1 / 32, 200, keep_density=True)
+    r = g["reflect_200"]
+    assert np.allclose(mom[0], r["m"], rtol=tol, atol=tol)
+    S, _ = orc.sigma(mom)
+    assert np.allclose([S[0, 0], S[0, 1], S[1, 1]], r["sigma"], rtol=tol)
+    assert abs(np.linalg.norm(dens) - r["l2_norm"]) <= 1e-12 * r["l2_norm"]
+    assert np.abs(dens[0][mask.astype(bool)]).max() == 0.0
+    ma = orc.solve(1, 1.0, 1.0, mask, [(4, 16)], 1 / 32, 200, outer_bc=1)
+    a = g["absorb_200"]
+    assert abs(ma[0, 0] - a["m00"]) <= tol
+    Sa, _ = orc.sigma(ma)
+    assert np.allclose([Sa[0, 0], Sa[0, 1], Sa[1, 1]], a["sigma"], rtol=tol)
+
+
+def test_errors(orc):
+    from oracle.oracle import OracleError
+    mask = c1_mask()
+    with pytest.raises(OracleError) as e:
+        orc.solve(1, 1.0, 1.0, mask, [(16, 16)], 1 / 32, 1)     # source inside the axon
+    assert e.value.code == 2
+    with pytest.raises(OracleError):
+        orc.solve(1, 1.0, 1.0, mask, [(40, 1)], 1 / 32, 1)      # out of grid
+    with pytest.raises(OracleError) as e:
+        orc.sigma(np.array([[0.0, 0, 0, 1, 0, 1]]))             # m00 <= 0
+    assert e.value.code == 6
+
+
+def test_own_mean_centering(orc):
+    """centering=1 shifts each density by its own mean (reading R12): then
+    Sigma = mean of per-source covariances."""
+    mask, src = _case(14)
+    mom = orc.solve(1, 1.0, 1.0, mask, src, 1 / 32, 64)
+    S1, mu1 = orc.sigma(mom, centering=1)
+    per = []
+    for m in mom:
+        ux, uy = m[1] / m[0], m[2] / m[0]
+        per.append([[m[3] / m[0] - ux * ux, m[4] / m[0] - ux * uy], [m[4] / m[0] - ux * uy, m[5] / m[0] - uy * uy]])
+    assert np.allclose(S1, np.mean(per, axis=0), rtol=1e-13)
+    assert np.allclose(mu1, 0)
