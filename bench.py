@@ -1,0 +1,304 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path on B200.
+
+One bench step = one pass of the whole hot path over one batch: Dirac data
+(K1), 32 SSP-RK3 steps (3 x K2 each), moments (K4), the moment all-reduce
+(N > 1) and Sigma (K5), through the C-ABI (dgdiff_solve_batch +
+dgdiff_covariance).  Workload: the c4 substrate (2048^2 Gamma axons, f = 0.60,
+seed 5), 256 sources per GPU per step drawn in order from the c4 source set
+(seed 6), P1, fp64 by default, dt = 1/32 (grid units h = D = 1).
+
+Metric (BASELINE.json): element-dof updates/s = sources x 2 nx ny d x nsteps
+/ time, whole job, all dofs (axon pixels included, as the paper's whole-domain
+solve counts them); the active-dof rate, Sigma solves/s and the stage
+kernel's HBM roofline fraction are reported beside it.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--precision 64|32]
+  python bench.py --impl reference ...   # the CPU oracle, bounded sample
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+NX = NY = 2048
+NSTEPS = 32
+DT = 1.0 / 32
+SRC_PER_GPU = 256
+METRIC = "element-dof updates/s"
+
+
+def workload_cfg(args, n_gpus):
+    return {
+        "workload": f"c4: {NX}x{NY} Gamma-axon substrate (f=0.60, seed 5), {SRC_PER_GPU} point sources per GPU per "
+                    f"step from the c4 source set (seed 6), P{args.degree}, dt=1/32, {NSTEPS} SSP-RK3 steps, "
+                    f"moments + Sigma",
+        "grid": [NX, NY],
+        "degree": args.degree,
+        "sources_per_step": SRC_PER_GPU * n_gpus,
+        "nsteps": NSTEPS,
+        "precision": args.precision,
+        "l2": "inputs larger than L2: the per-GPU state is ~62 GB (fp64) vs 126 MB L2",
+        "parallelism": f"dp{n_gpus} (sources sharded, one NCCL all-reduce of the moment table per step)",
+    }
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.rows = []
+        if self.p is None:
+            return
+        self.p.terminate()
+        try:
+            out, _ = self.p.communicate(timeout=5)
+        except Exception:
+            self.p.kill()
+            out = ""
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 9:
+                self.rows.append(f)
+
+    def summary(self):
+        if not getattr(self, "rows", None):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[5 + k].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ----------------------------------------------------------------------------- CPU oracle legs
+def oracle_sample(mask, sources, degree, nthreads, nsteps):
+    """Time the oracle (as it stands) on `len(sources)` sources x nsteps."""
+    from oracle import oracle as O
+    O.build()
+    t0 = time.perf_counter()
+    O.solve(degree, 1.0, 1.0, mask, sources, DT, nsteps, nthreads=nthreads)
+    return time.perf_counter() - t0
+
+
+def oracle_threads():
+    return max(1, min(os.cpu_count() or 1, 16))
+
+
+def cpu_baseline(mask, sources, degree):
+    th = oracle_threads()
+    nsteps = 2
+    src = sources[:th]
+    t = oracle_sample(mask, src, degree, th, nsteps)
+    d = (degree + 1) * (degree + 2) // 2
+    work = len(src) * 2 * NX * NY * d * nsteps
+    return {"value": work / t, "unit": METRIC, "cores": th, "kind": "oracle",
+            "sample": f"{len(src)} sources x {nsteps} SSP-RK3 steps on the same {NX}x{NY} c4 substrate "
+                      f"(O1 fp64, one OpenMP thread per source), {t:.1f} s wall"}
+
+
+def run_reference(args):
+    world, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    from paper_1907_06191_b200 import configs
+    mask = configs.mask("c4")
+    sources = configs.sources("c4")
+    th = oracle_threads()
+    d = (args.degree + 1) * (args.degree + 2) // 2
+    nsteps = 1
+    times = []
+    for k in range(args.warmup + args.steps):
+        src = sources[k * th:(k + 1) * th]
+        t = oracle_sample(mask, src, args.degree, th, nsteps)
+        if k >= args.warmup:
+            times.append(t)
+    work = th * 2 * NX * NY * d * nsteps
+    value = work * len(times) / sum(times)
+    sample = (f"per step: {th} sources x {nsteps} SSP-RK3 step on the {NX}x{NY} c4 substrate (O1 fp64, "
+              f"{th} OpenMP threads); the GPU arm's step is {SRC_PER_GPU} sources x {NSTEPS} steps")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "dof-updates/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload_cfg(args, world) | {"note": "bounded oracle sample"},
+            "cpu_baseline": {"value": value, "unit": "dof-updates/s", "cores": th, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "dof-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_ours(args):
+    import torch
+    world, rank, local = dist_env()
+    if world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1907_06191_b200 import configs
+    from paper_1907_06191_b200 import dgdiff as dg
+    mask = configs.mask("c4")
+    all_src = configs.sources("c4")
+    d = (args.degree + 1) * (args.degree + 2) // 2
+    nccl_id = None
+    if world > 1:
+        obj = [torch.cuda.nccl.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    stream = torch.cuda.current_stream()
+    solver = dg.Solver(mask, 1.0, 1.0, args.degree, precision=args.precision, rank=rank, nranks=world,
+                       nccl_id=nccl_id, stream=stream.cuda_stream, device=local, max_chunk=SRC_PER_GPU)
+    per_step = SRC_PER_GPU * world
+    dt = DT if args.degree == 1 else DT / 4
+    nsteps = NSTEPS
+
+    def batch(k):
+        off = (k * per_step) % (len(all_src) - per_step + 1)
+        return np.ascontiguousarray(all_src[off:off + per_step])
+
+    def step(k):
+        solver.solve(batch(k), dt, nsteps)
+        return solver.covariance()
+
+    for k in range(args.warmup):
+        step(k)
+    torch.cuda.synchronize()
+    dg.dgdiff_reset_stats(solver.handle)
+    dg.dgdiff_set_timing(solver.handle, 1)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        w0 = time.perf_counter()
+        ev0.record(stream)
+        for k in range(args.steps):
+            S, mu = step(args.warmup + k)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        w1 = time.perf_counter()
+    if dist:
+        dist.barrier()
+    dev_ms = ev0.elapsed_time(ev1)
+    wall_ms = (w1 - w0) * 1e3
+    st = dg.dgdiff_get_stats(solver.handle)
+    if dist:
+        t = torch.tensor([dev_ms, wall_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms, wall_ms = t.tolist()
+    total_src = per_step * args.steps
+    dofs = 2 * NX * NY * d
+    value = total_src * dofs * nsteps / (dev_ms * 1e-3)
+    e2e = total_src * dofs * nsteps / (wall_ms * 1e-3)
+    n_act = st["n_active"]
+    active = total_src * n_act * 2 * d * nsteps / (dev_ms * 1e-3)
+    peak, peak_src = peaks()
+    per_launch_bytes = st["stage_bytes"] / max(1, st["stage_launches"])
+    per_launch_ms = st["stage_ms"] / max(1, st["stage_launches"])
+    achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9 if per_launch_ms > 0 else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "stage_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            tj = json.load(f)
+        key = f"p{args.degree}_fp{args.precision}"
+        if key in tj:
+            traffic = tj[key]
+    line = {
+        "metric": METRIC, "value": value, "unit": "dof-updates/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64" if args.precision == 64 else "f32", "data": "synthetic",
+        "config": workload_cfg(args, world),
+        "active_dof_updates_per_s": active,
+        "sigma_solves_per_s": args.steps / (dev_ms * 1e-3),
+        "sigma_last": [S[0, 0], S[0, 1], S[1, 1]],
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "kernel": "k_stage (one SSP-RK3 stage)", "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": per_launch_bytes,
+                     "avg_launch_ms": per_launch_ms,
+                     "stage_share_of_step": st["stage_ms"] / dev_ms if dev_ms > 0 else None},
+        "e2e": {"value": e2e, "unit": "dof-updates/s", "h2d_bytes_per_step": st["h2d_bytes"],
+                "d2h_bytes_per_step": st["d2h_bytes"],
+                "note": "wall clock around dgdiff_solve_batch(host sources) + dgdiff_covariance(host Sigma)"},
+        "gpu_launches": st["launches"],
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(mask, all_src, args.degree)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    solver.close()
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--precision", type=int, default=64, choices=[64, 32])
+    ap.add_argument("--degree", type=int, default=1, choices=[1, 2])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("note: warmup < 3 violates the timing rules; using 3", file=sys.stderr)
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,169 @@
+/*
+ * dgdiff.h -- C-ABI of the B200-native hot path of arXiv 1907.06191
+ * ("DG-CUDA" diffusion covariance).  Paper = PAPER.md, cited as P:<line>.
+ *
+ * The library advances a batch of independent Dirac point sources
+ * by explicit SSP-RK3 steps of the paper's DG discretisation (Eq. (7),
+ * P:160-169; fluxes P:192-204; pixel mesh P:211) on a masked pixel substrate
+ * (axon pixels = k 0, Eq. (5)), reduces every density to its mass,
+ * first and second moments about its source point and combines them
+ * into the 2x2 covariance Sigma of the averaged Gaussian.
+ *
+ * Conventions (all functions):
+ *  - grid units are the caller's: pixel side h, diffusivity D, time dt;
+ *    pixel (i, j) covers [ih, (i+1)h] x [jh, (j+1)h]; arrays [ny][nx] are
+ *    row-major with i (x) fastest;
+ *  - every pointer argument is a HOST pointer; the library copies inputs and
+ *    writes outputs into caller buffers; the caller keeps ownership;
+ *  - a handle owns all of its device memory and, when nranks > 1, its NCCL
+ *    communicator; a handle is not thread-safe; separate handles are
+ *    independent;
+ *  - nothing throws across the ABI; every fallible call returns a
+ *    dgdiff_status and leaves a message for dgdiff_last_error();
+ *  - there is no CPU fallback: without a CUDA device dgdiff_create fails
+ *    with DGDIFF_E_CUDA.
+ */
+#ifndef DGDIFF_H
+#define DGDIFF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dgdiff_s *dgdiff_t; /* opaque */
+
+typedef enum {
+  DGDIFF_OK = 0,
+  DGDIFF_E_ARG = 1,        /* bad argument (sizes, degree, NULL, unsupported option) */
+  DGDIFF_E_SOURCE = 2,     /* a source pixel is outside the grid or masked */
+  DGDIFF_E_UNSTABLE = 3,   /* dt > dgdiff_dt_max(degree, h, D) */
+  DGDIFF_E_NONFINITE = 4,  /* NaN/Inf in the moments */
+  DGDIFF_E_STATE = 5,      /* call out of order, or delta != nsteps*dt */
+  DGDIFF_E_DEGENERATE = 6, /* a density with m00 <= 0 */
+  DGDIFF_E_CUDA = 7,       /* CUDA runtime error / no device */
+  DGDIFF_E_NCCL = 8,       /* NCCL missing or failed */
+  DGDIFF_E_NOMEM = 9       /* device allocation failed */
+} dgdiff_status;
+
+typedef struct {
+  int32_t precision;      /* 64 (default) or 32: arithmetic type of the state and
+                             of the stencil sum; moments always accumulate in fp64 */
+  int32_t outer_bc;       /* 0 = REFLECT (default): the outer square acts as an
+                             axon wall (reading R9).  1 = ABSORB, Eq. (4)
+                             (P:67-70): not implemented on the GPU path -> E_ARG */
+  int32_t centering;      /* 0 = shift each density by its source point (default,
+                             reading R12); 1 = by its own mean */
+  int32_t temporal_steps; /* 0 = library choice, 1 = one launch per RK stage,
+                             T_b > 1 = temporal-blocked kernel, T_b steps per pass */
+  int32_t device;         /* CUDA device ordinal; -1 = current device */
+  int32_t rank, nranks;   /* source sharding: rank takes the contiguous block
+                             [rank*n/nranks, (rank+1)*n/nranks) of every batch */
+  const void *nccl_id;    /* ncclUniqueId* (128 bytes), required iff nranks > 1 */
+  int32_t keep_density;   /* 1: keep the final states of the last source chunk for
+                             dgdiff_get_density (tests); 0 (default) */
+  int32_t max_chunk;      /* max sources resident per chunk; 0 = fit device memory */
+  void *stream;           /* cudaStream_t to launch on; NULL = a library stream */
+  int32_t kernel;         /* stage kernel variant: 0 = default (= 3); 1 = v1,
+                             operator table in global memory, global loads;
+                             2 = v2, operator as compile-time immediates, global
+                             loads; 3 = v3, row-marching shared-memory ring fed
+                             by bulk TMA.  Results agree to rounding; the
+                             state layout (and so the source-group size) differs:
+                             v1/v2 16-byte lanes, v3 8-byte lanes */
+} dgdiff_opts;
+
+/* Fill *o with the defaults above. */
+void dgdiff_opts_default(dgdiff_opts *o);
+
+/* Create a solver for one substrate.
+ *  mask   [ny][nx] uint8, 1 = axon pixel (k = 0, Eq. (5)), 0 = extracellular
+ *         (k = D); copied.
+ *  h, D   pixel side and extracellular diffusivity k0 (> 0).
+ *  degree Lagrange degree p of the triangle elements (Eq. (8); "p <= 3
+ *         suffices"): 1 or 2 (3 -> E_ARG in this version).
+ * Builds the operator tables (host), the open-face code of every pixel and the
+ * active-pixel index, copies them to the device; when nranks > 1 initialises
+ * NCCL from opts->nccl_id.  On failure *out is NULL. */
+dgdiff_status dgdiff_create(dgdiff_t *out, const uint8_t *mask, int32_t nx, int32_t ny, double h,
+                            double D, int32_t degree, const dgdiff_opts *opts);
+
+/* Step 1 of the scheme of P:239-243 for a batch of sources.
+ *  sources [n][2] int32 pixel indices (i, j); the Dirac sits at the pixel
+ *          centre ((i+1/2)h, (j+1/2)h); every rank passes the full list.
+ *  dt, nsteps  SSP-RK3 step and step count; the solve horizon is
+ *          Delta = nsteps*dt.  dt > dgdiff_dt_max -> E_UNSTABLE.
+ * On return (stream-ordered; the call itself does not synchronise with the
+ * device except for its host->device source copy) the per-source moments of
+ * this rank's shard are in the device moment table. */
+dgdiff_status dgdiff_solve_batch(dgdiff_t, const int32_t *sources, int64_t n, double dt,
+                                 int64_t nsteps);
+
+/* Steps 2-4 of P:243-265: centre + normalise each density, mix, and return
+ * the mixture's covariance.  delta must equal nsteps*dt of the last solve
+ * (relative 1e-12) -> else E_STATE.  When nranks > 1 this is the only
+ * collective: one ncclAllReduce(sum, fp64) of the zero-padded [n][6] moment
+ * table, after which every rank reduces the table in source order, so Sigma
+ * is bitwise identical for every nranks.  sigma[4] row-major (exactly
+ * symmetric), mu[2] (nullable) the mixture mean.  Synchronises. */
+dgdiff_status dgdiff_covariance(dgdiff_t, double delta, double sigma[4], double mu[2]);
+
+/* Per-source moments [n][6] = m00 m10 m01 m20 m11 m02 of the last solve,
+ * about each source point; rows of other ranks' shards are zero until
+ * dgdiff_covariance has run.  Synchronises. */
+dgdiff_status dgdiff_source_moments(dgdiff_t, double *out);
+
+/* Final state of source `src` of the last solve, in the canonical fp64 layout
+ * [ny][nx][2][d] (triangle 0 = L (0,0),(1,0),(1,1); 1 = U (0,0),(1,1),(0,1);
+ * nodes: vertices, then edge nodes of v0v1, v1v2, v2v0, then interior).
+ * Requires keep_density and src in this rank's last chunk -> else E_STATE. */
+dgdiff_status dgdiff_get_density(dgdiff_t, int64_t src, double *out);
+
+/* Largest stable SSP-RK3 step: 2.5127453 / rho_p * h^2 / D with the Bloch
+ * spectral radius rho_1 = 60, rho_2 = 192.7953 (reading R8);
+ * 0 for an unsupported degree. */
+double dgdiff_dt_max(int32_t degree, double h, double D);
+
+/* Thread-local message of the last failing call ("" if none). */
+const char *dgdiff_last_error(void);
+
+/* NULL-safe. */
+void dgdiff_destroy(dgdiff_t);
+
+/* ---- host-only introspection (no device needed) ------------------------ */
+
+/* The composite stencil of the semi-discrete operator after eliminating q,
+ * in units of D/h^2, for degree p (1, 2):  A [16][5][2d][2d] with
+ * code bit0 = E open, bit1 = W, bit2 = N, bit3 = S and offsets
+ * 0 self, 1 E (+1,0), 2 W (-1,0), 3 N (0,+1), 4 S (0,-1); rows = outputs,
+ * columns = the neighbour's dofs in canonical order (triangle-major).
+ *  W    [2][6][d]: int over the unit pixel's triangle of xi^a eta^b N_j,
+ *       (a,b) = 00,10,01,20,11,02.
+ *  init [2][d]:  the projected Dirac at the pixel centre times h^2.
+ * Any pointer may be NULL. */
+dgdiff_status dgdiff_operator_table(int32_t degree, double *A, double *W, double *init);
+
+/* Source shard of `rank` out of `nranks` for a batch of n sources. */
+void dgdiff_shard(int64_t n, int32_t rank, int32_t nranks, int64_t *begin, int64_t *end);
+
+typedef struct {
+  int64_t launches;        /* kernels launched by this handle so far */
+  int64_t stage_launches;  /* of which RK-stage (or temporal-blocked) launches */
+  double stage_ms;         /* summed device time of those launches (CUDA events on
+                              the launch stream), if timing is enabled */
+  double stage_bytes;      /* algorithmic HBM bytes of those launches */
+  int64_t n_active;        /* extracellular pixels */
+  int64_t chunk;           /* sources per chunk of the last solve */
+  int64_t h2d_bytes, d2h_bytes; /* host<->device bytes moved by the last solve+covariance */
+} dgdiff_stats_t;
+
+/* Enable (1) / disable (0) CUDA-event timing of the stage launches. */
+dgdiff_status dgdiff_set_timing(dgdiff_t, int32_t enable);
+dgdiff_status dgdiff_get_stats(dgdiff_t, dgdiff_stats_t *out);
+dgdiff_status dgdiff_reset_stats(dgdiff_t);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DGDIFF_H */

@@ -1,0 +1,963 @@
+// dgdiff.cu -- C-ABI (include/dgdiff.h), host driver and sm_100a kernels of the
+// hot path of arXiv 1907.06191 (PAPER.md, cited P:<line>).
+//
+//   K1 k_init      Dirac Cauchy data for a chunk of sources
+//   K2 k_stage     one SSP-RK3 stage of the DG operator (Eq. (7))
+//                  as a 5-point composite stencil over extracellular pixels
+//   K3 k_stage_tb  (temporal blocking, see stage_tb.cuh)
+//   K4 k_moments   m00 m10 m01 m20 m11 m02 per source
+//   K5 k_finalize  mixture mean and covariance Sigma; preceded by
+//                  one ncclAllReduce of the moment table when nranks > 1
+//
+// No CPU fallback exists: every step of the path runs in these kernels.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/dgdiff.h"
+#include "kernels.cuh"
+#include "operator.h"
+#include "stage_imm.cuh"
+#include "stage_ring.cuh"
+
+using namespace dgk;
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+static thread_local std::string g_err;
+static dgdiff_status fail(dgdiff_status s, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+#define CK(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess)                                                                 \
+      return fail(e_ == cudaErrorMemoryAllocation ? DGDIFF_E_NOMEM : DGDIFF_E_CUDA,        \
+                  "%s: %s (%s:%d)", #x, cudaGetErrorString(e_), __FILE__, __LINE__);       \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// device constants
+// ---------------------------------------------------------------------------
+#define DMAXK 6                    // max dofs per triangle on the GPU path (P2)
+__constant__ double c_W[2 * 6 * DMAXK];    // moment weights (unit pixel)
+
+struct InitVals { double v[2 * DMAXK]; };  // projected Dirac / h^2
+
+// ---------------------------------------------------------------------------
+// K1: zero the chunk's u and write the projected Dirac at each source pixel
+// ---------------------------------------------------------------------------
+template <typename T, int NV, int D2>
+__global__ void __launch_bounds__(256) k_init(T *__restrict__ U, int64_t nvec, int nact,
+                                              const int *__restrict__ src_a, InitVals iv) {
+  constexpr int G = 32 * NV;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    int lane = (int)(v & 31);
+    int64_t r = v >> 5;               // (g, a, k)
+    int k = (int)(r % D2);
+    int64_t ga = r / D2;
+    int a = (int)(ga % nact);
+    int64_t g = ga / nact;
+    T x[NV];
+#pragma unroll
+    for (int e = 0; e < NV; e++) {
+      int s = (int)(g * G + lane * NV + e);
+      x[e] = (__ldg(&src_a[s]) == a) ? (T)iv.v[k] : (T)0;
+    }
+    stv<T, NV>(U + v * NV, x);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2: one RK stage,  Uout = Uin + alpha (U0 - Uin) + cs * sum_o A[code][o] Uin[p+o]
+// A in units D/h^2 (exact dyadic); cs = beta dt D/h^2 applied after the sum
+// (SURVEY F4/F9).  One warp = one pixel x G sources; a CTA = WPB source groups
+// of one contiguous range of pixels (pixel index uniform over the CTA).
+// U0 may alias Uout (stage 3 writes u in place: same element, same thread).
+// ---------------------------------------------------------------------------
+template <typename T, int NV, int D2>
+__device__ __forceinline__ void block_mv(T (&acc)[D2][NV], const T *__restrict__ Ab, const T (&x)[D2][NV]) {
+#pragma unroll
+  for (int r = 0; r < D2; r++)
+#pragma unroll
+    for (int c = 0; c < D2; c++) {
+      T a = __ldg(Ab + r * D2 + c);
+#pragma unroll
+      for (int e = 0; e < NV; e++) acc[r][e] = fma(a, x[c][e], acc[r][e]);
+    }
+}
+
+template <typename T, int NV, int D2, bool HAS_ALPHA>
+__global__ void __launch_bounds__(256) k_stage(const T *__restrict__ Uin, const T *U0, T *Uout,
+                                               const int4 *__restrict__ nbr, const T *__restrict__ A,
+                                               int nact, int ngroups, int px_per_cta, T alpha, T cs) {
+  constexpr int G = 32 * NV;
+  const int lane = threadIdx.x & 31;
+  const int g = blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (g >= ngroups) return;
+  const size_t gofs = (size_t)g * nact * D2 * G + lane * NV;
+  const T *Ug = Uin + gofs;
+  const int a0 = blockIdx.x * px_per_cta;
+  const int a1 = min(nact, a0 + px_per_cta);
+  for (int a = a0; a < a1; a++) {
+    const int4 nb = __ldg(&nbr[a]);
+    const int code = open_code(nb);
+    const T *Ac = A + (size_t)code * 5 * D2 * D2;
+    T xs[D2][NV], acc[D2][NV];
+#pragma unroll
+    for (int k = 0; k < D2; k++) ldv<T, NV>(Ug + ((size_t)a * D2 + k) * G, xs[k]);
+#pragma unroll
+    for (int k = 0; k < D2; k++)
+#pragma unroll
+      for (int e = 0; e < NV; e++) acc[k][e] = (T)0;
+    block_mv<T, NV, D2>(acc, Ac, xs);
+    const int nbi[4] = {nb.x, nb.y, nb.z, nb.w};
+#pragma unroll
+    for (int o = 0; o < 4; o++) {
+      if (nbi[o] < 0) continue;  // closed face: neighbour is axon / outside, u+ = 0
+      T xn[D2][NV];
+#pragma unroll
+      for (int k = 0; k < D2; k++) ldv<T, NV>(Ug + ((size_t)nbi[o] * D2 + k) * G, xn[k]);
+      block_mv<T, NV, D2>(acc, Ac + (o + 1) * D2 * D2, xn);
+    }
+    T *out = Uout + gofs + (size_t)a * D2 * G;
+    const T *u0 = U0 + gofs + (size_t)a * D2 * G;
+#pragma unroll
+    for (int k = 0; k < D2; k++) {
+      T y[NV];
+      if (HAS_ALPHA) {
+        T z[NV];
+        ldvc<T, NV>(u0 + (size_t)k * G, z);
+#pragma unroll
+        for (int e = 0; e < NV; e++) y[e] = xs[k][e] + alpha * (z[e] - xs[k][e]) + cs * acc[k][e];
+      } else {
+#pragma unroll
+        for (int e = 0; e < NV; e++) y[e] = xs[k][e] + cs * acc[k][e];
+      }
+      stv<T, NV>(out + (size_t)k * G, y);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K4: per-source moments about the source pixel centre (readings R12, R14):
+//   m_ab = h^(2+a+b) sum_pixels sum_T sum_j c_j int (xi+X)^a (eta+Y)^b N_j
+// with X = i - is - 1/2, Y = j - js - 1/2.  fp64 accumulation.  Each CTA
+// reduces a contiguous pixel range; k_mom_reduce then sums the per-CTA
+// partials in CTA order (deterministic, independent of chunking and ranks).
+// ---------------------------------------------------------------------------
+template <typename T, int NV, int D2>
+__global__ void __launch_bounds__(256) k_moments(const T *__restrict__ U, const int2 *__restrict__ pix,
+                                                 const int2 *__restrict__ src_ij, int nact, int ngroups,
+                                                 int px_per_cta, double *__restrict__ partial,
+                                                 int64_t chunk) {
+  constexpr int G = 32 * NV, d = D2 / 2;
+  const int lane = threadIdx.x & 31;
+  const int g = blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (g >= ngroups) return;
+  const T *Ug = U + (size_t)g * nact * D2 * G + lane * NV;
+  double is[NV], js[NV], m[6][NV];
+#pragma unroll
+  for (int e = 0; e < NV; e++) {
+    int2 s = __ldg(&src_ij[g * G + lane * NV + e]);
+    is[e] = s.x + 0.5;
+    js[e] = s.y + 0.5;
+#pragma unroll
+    for (int q = 0; q < 6; q++) m[q][e] = 0.0;
+  }
+  const int a0 = blockIdx.x * px_per_cta;
+  const int a1 = min(nact, a0 + px_per_cta);
+  for (int a = a0; a < a1; a++) {
+    const int2 ij = __ldg(&pix[a]);
+    T c[D2][NV];
+#pragma unroll
+    for (int k = 0; k < D2; k++) ldv<T, NV>(Ug + ((size_t)a * D2 + k) * G, c[k]);
+#pragma unroll
+    for (int e = 0; e < NV; e++) {
+      double P[6] = {0, 0, 0, 0, 0, 0};
+#pragma unroll
+      for (int t = 0; t < 2; t++)
+#pragma unroll
+        for (int q = 0; q < 6; q++)
+#pragma unroll
+          for (int j = 0; j < d; j++) P[q] = fma(c_W[(t * 6 + q) * DMAXK + j], (double)c[t * d + j][e], P[q]);
+      const double X = ij.x - is[e], Y = ij.y - js[e];
+      m[0][e] += P[0];
+      m[1][e] += P[1] + X * P[0];
+      m[2][e] += P[2] + Y * P[0];
+      m[3][e] += P[3] + 2.0 * X * P[1] + X * X * P[0];
+      m[4][e] += P[4] + X * P[2] + Y * P[1] + X * Y * P[0];
+      m[5][e] += P[5] + 2.0 * Y * P[2] + Y * Y * P[0];
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < NV; e++) {
+    double *o = partial + ((size_t)blockIdx.x * chunk + g * G + lane * NV + e) * 6;
+#pragma unroll
+    for (int q = 0; q < 6; q++) o[q] = m[q][e];
+  }
+}
+
+// sum the partials in CTA order; scale by h powers; write rows of the table
+__global__ void k_mom_reduce(const double *__restrict__ partial, int nblk, int64_t chunk, int64_t nvalid,
+                             double h, double *__restrict__ mom /* rows of this chunk */) {
+  int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= nvalid) return;
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+  for (int b = 0; b < nblk; b++) {
+    const double *p = partial + ((size_t)b * chunk + s) * 6;
+#pragma unroll
+    for (int q = 0; q < 6; q++) acc[q] += p[q];
+  }
+  const double h2 = h * h, h3 = h2 * h, h4 = h2 * h2;
+  double *o = mom + s * 6;
+  o[0] = acc[0] * h2;
+  o[1] = acc[1] * h3;
+  o[2] = acc[2] * h3;
+  o[3] = acc[3] * h4;
+  o[4] = acc[4] * h4;
+  o[5] = acc[5] * h4;
+}
+
+// ---------------------------------------------------------------------------
+// K5: mixture and its covariance from the full
+// [n][6] table, fixed-order reduction (bitwise identical on every rank).
+// out[0..5] = sxx sxy syy mux muy flags (bit0 degenerate, bit1 non-finite)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_finalize(const double *__restrict__ mom, int64_t n, int centering,
+                                                  double *__restrict__ out) {
+  __shared__ double sh[5][256];
+  __shared__ int shf[256];
+  const int t = threadIdx.x;
+  const int64_t b = n * t / 256, e = n * (t + 1) / 256;
+  double s[5] = {0, 0, 0, 0, 0};
+  int flag = 0;
+  for (int64_t i = b; i < e; i++) {
+    const double *m = mom + i * 6;
+    if (!(m[0] > 0)) flag |= isfinite(m[0]) ? 1 : 2;
+    double ux = m[1] / m[0], uy = m[2] / m[0];  // centring + normalisation
+    double xx = m[3] / m[0], xy = m[4] / m[0], yy = m[5] / m[0];
+    if (centering == 1) { xx -= ux * ux; xy -= ux * uy; yy -= uy * uy; ux = 0; uy = 0; }
+    s[0] += ux; s[1] += uy; s[2] += xx; s[3] += xy; s[4] += yy;
+  }
+  for (int q = 0; q < 5; q++) sh[q][t] = s[q];
+  shf[t] = flag;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (t < w) {
+      for (int q = 0; q < 5; q++) sh[q][t] += sh[q][t + w];
+      shf[t] |= shf[t + w];
+    }
+    __syncthreads();
+  }
+  if (t == 0) {
+    double inv = 1.0 / (double)n;
+    double mx = sh[0][0] * inv, my = sh[1][0] * inv;
+    out[0] = sh[2][0] * inv - mx * mx;
+    out[1] = sh[3][0] * inv - mx * my;
+    out[2] = sh[4][0] * inv - my * my;
+    out[3] = mx;
+    out[4] = my;
+    int f = shf[0];
+    for (int q = 0; q < 3; q++)
+      if (!isfinite(out[q])) f |= 2;
+    out[5] = (double)f;
+  }
+}
+
+// canonical fp64 copy of one source's state: out[a][k]
+template <typename T, int NV, int D2>
+__global__ void k_gather(const T *__restrict__ U, int nact, int g, int slot, double *__restrict__ out) {
+  constexpr int G = 32 * NV;
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= (int64_t)nact * D2) return;
+  out[r] = (double)U[((size_t)g * nact * D2 + r) * G + slot];
+}
+
+// source pixel -> active index for a chunk (padding slots repeat source 0)
+__global__ void k_src_prep(const int32_t *__restrict__ src, int64_t nvalid, int64_t chunk,
+                           const int *__restrict__ aidx, int nx, int *__restrict__ src_a,
+                           int2 *__restrict__ src_ij) {
+  int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= chunk) return;
+  int64_t k = s < nvalid ? s : 0;
+  int i = src[2 * k], j = src[2 * k + 1];
+  src_a[s] = aidx[(size_t)j * nx + i];
+  src_ij[s] = make_int2(i, j);
+}
+
+// ---------------------------------------------------------------------------
+// NCCL (dlopen'ed: only needed when nranks > 1)
+// ---------------------------------------------------------------------------
+struct NcclApi {
+  void *h = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char *(*errStr)(ncclResult_t) = nullptr;
+  bool load() {
+    if (h) return true;
+    const char *names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char *nm : names)
+      if ((h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (!h) return false;
+    commInitRank = (decltype(commInitRank))dlsym(h, "ncclCommInitRank");
+    allReduce = (decltype(allReduce))dlsym(h, "ncclAllReduce");
+    commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
+    errStr = (decltype(errStr))dlsym(h, "ncclGetErrorString");
+    return commInitRank && allReduce && commDestroy && errStr;
+  }
+};
+static NcclApi g_nccl;
+
+// ---------------------------------------------------------------------------
+// handle
+// ---------------------------------------------------------------------------
+struct dgdiff_s {
+  int nx = 0, ny = 0, p = 1, d = 3, D2 = 6;
+  double h = 1, D = 1;
+  dgdiff_opts o;
+  int dev = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int64_t nact = 0;
+  int4 *d_nbr = nullptr;
+  int4 *d_rowtab = nullptr;  // [nstrips][ny] {h0, c0, c1, h1} for the ring kernel
+  int nstrips = 0, ring_w = 0, nsm = 148;
+  int2 *d_pix = nullptr;
+  int *d_aidx = nullptr;
+  std::vector<int> h_aidx;
+  void *d_A = nullptr;
+  dgop::Table tab;
+  // chunk buffers
+  void *d_U[3] = {nullptr, nullptr, nullptr};
+  int64_t chunk_cap = 0;  // sources the U buffers hold
+  int *d_src_a = nullptr;
+  int2 *d_src_ij = nullptr;
+  double *d_partial = nullptr;
+  size_t partial_cap = 0;
+  int32_t *d_src = nullptr;
+  int64_t src_cap = 0;
+  double *d_mom = nullptr;
+  int64_t mom_cap = 0;
+  double *d_out = nullptr;
+  // last solve
+  bool solved = false;
+  int64_t last_n = 0, last_nsteps = 0;
+  double last_dt = 0;
+  int64_t last_chunk_begin = -1, last_chunk_n = 0;  // global source index range kept (keep_density)
+  int64_t last_chunk_size = 0;
+  // NCCL
+  ncclComm_t comm = nullptr;
+  // stats
+  dgdiff_stats_t st;
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  size_t ev_used = 0;
+  int64_t ev_launches_pending = 0;
+};
+
+static size_t tsize(const dgdiff_s *H) { return H->o.precision == 32 ? 4 : 8; }
+// lane width of the state layout: 16 B for the global-load kernels (v1, v2),
+// 8 B for the row-ring kernel (v3, default) so that four full row tiles fit
+static int lane_bytes(const dgdiff_s *H) { return (H->o.kernel == 1 || H->o.kernel == 2) ? 16 : 8; }
+static int gsize(const dgdiff_s *H) { return 32 * lane_bytes(H) / (int)tsize(H); }
+static bool use_ring(const dgdiff_s *H) { return !(H->o.kernel == 1 || H->o.kernel == 2); }
+
+extern "C" void dgdiff_opts_default(dgdiff_opts *o) {
+  if (!o) return;
+  memset(o, 0, sizeof(*o));
+  o->precision = 64;
+  o->outer_bc = 0;
+  o->centering = 0;
+  o->temporal_steps = 0;
+  o->device = -1;
+  o->rank = 0;
+  o->nranks = 1;
+  o->nccl_id = nullptr;
+  o->keep_density = 0;
+  o->max_chunk = 0;
+  o->stream = nullptr;
+  o->kernel = 0;
+}
+
+extern "C" const char *dgdiff_last_error(void) { return g_err.c_str(); }
+
+extern "C" double dgdiff_dt_max(int32_t degree, double h, double D) {
+  // SSP-RK3 real-axis stability limit 2.5127453 over the Bloch spectral radius
+  // of the composite operator (R8): rho_1 = 60, rho_2 = 192.7953
+  double rho = degree == 1 ? 60.0 : degree == 2 ? 192.7953 : 0.0;
+  if (rho == 0.0 || !(h > 0) || !(D > 0)) return 0.0;
+  return 2.5127453 / rho * h * h / D;
+}
+
+extern "C" void dgdiff_shard(int64_t n, int32_t rank, int32_t nranks, int64_t *begin, int64_t *end) {
+  if (nranks < 1) nranks = 1;
+  if (rank < 0) rank = 0;
+  if (rank >= nranks) rank = nranks - 1;
+  if (begin) *begin = n * rank / nranks;
+  if (end) *end = n * (rank + 1) / nranks;
+}
+
+extern "C" dgdiff_status dgdiff_operator_table(int32_t degree, double *A, double *W, double *init) {
+  if (degree < 1 || degree > 2) return fail(DGDIFF_E_ARG, "degree %d not supported (1 or 2)", degree);
+  try {
+    dgop::Table T = dgop::build(degree);
+    if (A) memcpy(A, T.A.data(), T.A.size() * sizeof(double));
+    if (W) memcpy(W, T.W.data(), T.W.size() * sizeof(double));
+    if (init) memcpy(init, T.init.data(), T.init.size() * sizeof(double));
+  } catch (std::exception &e) {
+    return fail(DGDIFF_E_ARG, "operator precompute failed: %s", e.what());
+  }
+  return DGDIFF_OK;
+}
+
+static void release(dgdiff_s *H) {
+  if (!H) return;
+  for (auto &p : H->ev) {
+    cudaEventDestroy(p.first);
+    cudaEventDestroy(p.second);
+  }
+  for (int r = 0; r < 3; r++) cudaFree(H->d_U[r]);
+  cudaFree(H->d_nbr);
+  cudaFree(H->d_rowtab);
+  cudaFree(H->d_pix);
+  cudaFree(H->d_aidx);
+  cudaFree(H->d_A);
+  cudaFree(H->d_src_a);
+  cudaFree(H->d_src_ij);
+  cudaFree(H->d_partial);
+  cudaFree(H->d_src);
+  cudaFree(H->d_mom);
+  cudaFree(H->d_out);
+  if (H->comm && g_nccl.commDestroy) g_nccl.commDestroy(H->comm);
+  if (H->own_stream && H->stream) cudaStreamDestroy(H->stream);
+  delete H;
+}
+
+extern "C" void dgdiff_destroy(dgdiff_t H) {
+  if (!H) return;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(H->dev);
+  release(H);
+  cudaSetDevice(cur);
+}
+
+static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
+  const int nx = H->nx, ny = H->ny;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return fail(DGDIFF_E_CUDA, "no CUDA device (%s): the GPU path has no CPU fallback",
+                e != cudaSuccess ? cudaGetErrorString(e) : "count 0");
+  if (H->o.device >= 0) {
+    if (H->o.device >= ndev) return fail(DGDIFF_E_ARG, "device %d of %d", H->o.device, ndev);
+    CK(cudaSetDevice(H->o.device));
+  }
+  CK(cudaGetDevice(&H->dev));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, H->dev));
+  if (prop.major < 10)
+    return fail(DGDIFF_E_CUDA, "device %s is sm_%d%d; this library is built for sm_100a", prop.name,
+                prop.major, prop.minor);
+  if (H->o.stream) {
+    H->stream = (cudaStream_t)H->o.stream;
+  } else {
+    CK(cudaStreamCreateWithFlags(&H->stream, cudaStreamNonBlocking));
+    H->own_stream = true;
+  }
+  // K0 operator tables
+  try {
+    H->tab = dgop::build(H->p);
+  } catch (std::exception &ex) {
+    return fail(DGDIFF_E_ARG, "operator precompute failed: %s", ex.what());
+  }
+  // the kernels carry the operator as compile-time immediates (tables.inc,
+  // generated from K0 at build time): check them against this run's K0
+  {
+    const int D2 = H->D2;
+    auto A = [&](int code, int o, int r, int c) { return H->tab.A[(((size_t)code * 5 + o) * D2 + r) * D2 + c]; };
+    for (int code = 0; code < 16; code++)
+      for (int r = 0; r < D2; r++)
+        for (int c = 0; c < D2; c++) {
+          auto tb = [&](int b) { return H->p == 1 ? dgk::tab<1>(b, r, c) : dgk::tab<2>(b, r, c); };
+          double self = tb(0);
+          for (int f = 0; f < 4; f++)
+            if ((code >> f) & 1) self += tb(1 + f);
+          if (self != A(code, 0, r, c)) return fail(DGDIFF_E_ARG, "compiled operator table differs from K0 (self)");
+          for (int f = 0; f < 4; f++)
+            if (A(code, 1 + f, r, c) != (((code >> f) & 1) ? tb(5 + f) : 0.0))
+              return fail(DGDIFF_E_ARG, "compiled operator table differs from K0 (neighbour)");
+        }
+  }
+  // active pixels in raster order, their open-face neighbours (out of grid
+  // counts as axon under REFLECT, reading R9)
+  std::vector<int> aidx((size_t)nx * ny, -1);
+  std::vector<int2> pix;
+  for (int j = 0; j < ny; j++)
+    for (int i = 0; i < nx; i++)
+      if (!mask[(size_t)j * nx + i]) {
+        aidx[(size_t)j * nx + i] = (int)pix.size();
+        pix.push_back(make_int2(i, j));
+      }
+  H->nact = (int64_t)pix.size();
+  H->h_aidx = aidx;
+  if (H->nact == 0) return fail(DGDIFF_E_ARG, "substrate has no extracellular pixel");
+  std::vector<int4> nbr(H->nact);
+  auto at = [&](int i, int j) { return (i < 0 || j < 0 || i >= nx || j >= ny) ? -1 : aidx[(size_t)j * nx + i]; };
+  for (int64_t a = 0; a < H->nact; a++) {
+    int i = pix[a].x, j = pix[a].y;
+    nbr[a] = make_int4(at(i + 1, j), at(i - 1, j), at(i, j + 1), at(i, j - 1));
+  }
+  // ring kernel row table: active-index bounds of every (strip, row) tile
+  if (use_ring(H)) {
+    H->ring_w = H->p == 1 ? RingCfg<1>::W : RingCfg<2>::W;
+    const int W = H->ring_w;
+    H->nstrips = (nx + W - 1) / W;
+    std::vector<int> cum((size_t)ny * (nx + 1));
+    int run = 0;
+    for (int j = 0; j < ny; j++) {
+      for (int i = 0; i < nx; i++) {
+        cum[(size_t)j * (nx + 1) + i] = run;
+        if (!mask[(size_t)j * nx + i]) run++;
+      }
+      cum[(size_t)j * (nx + 1) + nx] = run;
+    }
+    std::vector<int4> rtab((size_t)H->nstrips * ny);
+    for (int s = 0; s < H->nstrips; s++)
+      for (int j = 0; j < ny; j++) {
+        const int x0 = s * W;
+        auto c = [&](int x) { return cum[(size_t)j * (nx + 1) + std::max(0, std::min(nx, x))]; };
+        rtab[(size_t)s * ny + j] = make_int4(c(x0 - 1), c(x0), c(x0 + W), c(x0 + W + 1));
+      }
+    CK(cudaMalloc(&H->d_rowtab, sizeof(int4) * rtab.size()));
+    CK(cudaMemcpy(H->d_rowtab, rtab.data(), sizeof(int4) * rtab.size(), cudaMemcpyHostToDevice));
+  }
+  H->nsm = prop.multiProcessorCount;
+  CK(cudaMalloc(&H->d_nbr, sizeof(int4) * H->nact));
+  CK(cudaMalloc(&H->d_pix, sizeof(int2) * H->nact));
+  CK(cudaMalloc(&H->d_aidx, sizeof(int) * (size_t)nx * ny));
+  CK(cudaMemcpy(H->d_nbr, nbr.data(), sizeof(int4) * H->nact, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(H->d_pix, pix.data(), sizeof(int2) * H->nact, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(H->d_aidx, aidx.data(), sizeof(int) * (size_t)nx * ny, cudaMemcpyHostToDevice));
+  // operator table in the state precision (exact: dyadic entries)
+  size_t na = H->tab.A.size();
+  if (H->o.precision == 32) {
+    std::vector<float> A32(na);
+    for (size_t k = 0; k < na; k++) A32[k] = (float)H->tab.A[k];
+    CK(cudaMalloc(&H->d_A, na * sizeof(float)));
+    CK(cudaMemcpy(H->d_A, A32.data(), na * sizeof(float), cudaMemcpyHostToDevice));
+  } else {
+    CK(cudaMalloc(&H->d_A, na * sizeof(double)));
+    CK(cudaMemcpy(H->d_A, H->tab.A.data(), na * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  double W[2 * 6 * DMAXK] = {0};
+  for (int t = 0; t < 2; t++)
+    for (int q = 0; q < 6; q++)
+      for (int j = 0; j < H->d; j++) W[(t * 6 + q) * DMAXK + j] = H->tab.W[(t * 6 + q) * H->d + j];
+  CK(cudaMemcpyToSymbol(c_W, W, sizeof W));
+  CK(cudaMalloc(&H->d_out, 8 * sizeof(double)));
+  // NCCL
+  if (H->o.nranks > 1) {
+    if (!H->o.nccl_id) return fail(DGDIFF_E_ARG, "nranks > 1 needs opts.nccl_id");
+    if (!g_nccl.load()) return fail(DGDIFF_E_NCCL, "cannot load libnccl.so.2: %s", dlerror());
+    ncclUniqueId id;
+    memcpy(&id, H->o.nccl_id, sizeof id);
+    ncclResult_t r = g_nccl.commInitRank(&H->comm, H->o.nranks, id, H->o.rank);
+    if (r != ncclSuccess) return fail(DGDIFF_E_NCCL, "ncclCommInitRank: %s", g_nccl.errStr(r));
+  }
+  H->st.n_active = H->nact;
+  return DGDIFF_OK;
+}
+
+extern "C" dgdiff_status dgdiff_create(dgdiff_t *out, const uint8_t *mask, int32_t nx, int32_t ny, double h,
+                                       double D, int32_t degree, const dgdiff_opts *opts) {
+  if (!out) return fail(DGDIFF_E_ARG, "out is NULL");
+  *out = nullptr;
+  if (!mask || nx < 1 || ny < 1) return fail(DGDIFF_E_ARG, "mask NULL or empty grid %dx%d", nx, ny);
+  if ((int64_t)nx * ny >= (1LL << 31)) return fail(DGDIFF_E_ARG, "grid too large");
+  if (!(h > 0) || !(D > 0) || !std::isfinite(h) || !std::isfinite(D))
+    return fail(DGDIFF_E_ARG, "h and D must be positive and finite");
+  if (degree < 1 || degree > 2) return fail(DGDIFF_E_ARG, "degree %d not supported (1 or 2)", degree);
+  dgdiff_opts o;
+  if (opts) o = *opts; else dgdiff_opts_default(&o);
+  if (o.precision != 32 && o.precision != 64) return fail(DGDIFF_E_ARG, "precision must be 32 or 64");
+  if (o.outer_bc != 0)
+    return fail(DGDIFF_E_ARG, "outer_bc ABSORB (Eq. (4)) is not implemented on the GPU path; REFLECT only");
+  if (o.centering != 0 && o.centering != 1) return fail(DGDIFF_E_ARG, "centering must be 0 or 1");
+  if (o.nranks < 1 || o.rank < 0 || o.rank >= o.nranks) return fail(DGDIFF_E_ARG, "bad rank/nranks");
+  if (o.temporal_steps < 0) return fail(DGDIFF_E_ARG, "temporal_steps < 0");
+  if (o.max_chunk < 0) return fail(DGDIFF_E_ARG, "max_chunk < 0");
+  dgdiff_s *H = new dgdiff_s();
+  H->nx = nx; H->ny = ny; H->h = h; H->D = D; H->p = degree;
+  H->d = (degree + 1) * (degree + 2) / 2;
+  H->D2 = 2 * H->d;
+  H->o = o;
+  memset(&H->st, 0, sizeof H->st);
+  dgdiff_status s = create_impl(H, mask);
+  if (s != DGDIFF_OK) {
+    release(H);
+    return s;
+  }
+  *out = H;
+  return DGDIFF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// solve
+// ---------------------------------------------------------------------------
+template <typename T, int NV, int P, bool ALPHA>
+static cudaError_t launch_ring(dgdiff_s *H, const T *Uin, const T *U0, T *Uout, int ngroups, T alpha, T cs) {
+  using Gm = RingGeom<T, NV, P>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_stage_ring<T, NV, P, ALPHA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Gm::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int ny = H->ny;
+  const int per_band = H->nstrips * ngroups;
+  int nbands = std::max(1, std::min(ny, (8 * H->nsm + per_band - 1) / per_band));
+  int band_rows = (ny + nbands - 1) / nbands;
+  if (band_rows > RING_MAXBAND) band_rows = RING_MAXBAND;
+  nbands = (ny + band_rows - 1) / band_rows;
+  const int nitems = per_band * nbands;
+  const int grid = std::min(nitems, H->nsm);
+  k_stage_ring<T, NV, P, ALPHA><<<grid, Gm::W * 32, Gm::SMEM, H->stream>>>(
+      Uin, U0, Uout, H->d_nbr, H->d_rowtab, (int)H->nact, ny, H->nstrips, ngroups, band_rows, nitems, alpha, cs);
+  return cudaGetLastError();
+}
+
+template <typename T, int NV, int D2>
+static dgdiff_status run_chunk(dgdiff_s *H, int64_t nvalid, int64_t chunk, double dt, int64_t nsteps,
+                               double *mom_rows) {
+  constexpr int G = 32 * NV;
+  const int ngroups = (int)(chunk / G);
+  const int nact = (int)H->nact;
+  cudaStream_t st = H->stream;
+  T *u = (T *)H->d_U[0], *Ua = (T *)H->d_U[1], *Ub = (T *)H->d_U[2];
+  // K1
+  InitVals iv;
+  const double ih2 = 1.0 / (H->h * H->h);
+  for (int k = 0; k < D2; k++) iv.v[k] = H->tab.init[k] * ih2;
+  int64_t nvec = (int64_t)ngroups * nact * D2 * 32;
+  int blocks = (int)std::min<int64_t>((nvec + 255) / 256, 148 * 64);
+  k_init<T, NV, D2><<<blocks, 256, 0, st>>>(u, nvec, nact, H->d_src_a, iv);
+  H->st.launches++;
+  // K2 x 3 per step (SSP-RK3 increment form, R7)
+  const int wpb = std::min(ngroups, 4);
+  const int px = 32;
+  dim3 grid((nact + px - 1) / px, (ngroups + wpb - 1) / wpb);
+  const double c = dt * H->D / (H->h * H->h);
+  const T a2 = (T)0.75, a3 = (T)(1.0 / 3.0);
+  const T c1 = (T)c, c2 = (T)(0.25 * c), c3 = (T)((2.0 / 3.0) * c);
+  const T *A = (const T *)H->d_A;
+  const double pass = (double)nact * D2 * chunk * sizeof(T);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (H->timing && nsteps > 0) {
+    if (H->ev_used == H->ev.size()) {
+      cudaEvent_t a, b;
+      CK(cudaEventCreate(&a));
+      CK(cudaEventCreate(&b));
+      H->ev.push_back({a, b});
+    }
+    e0 = H->ev[H->ev_used].first;
+    e1 = H->ev[H->ev_used].second;
+    H->ev_used++;
+    CK(cudaEventRecord(e0, st));
+  }
+  constexpr int P = D2 == 6 ? 1 : 2;
+  if constexpr (NV * sizeof(T) == 16) {
+    if (H->o.kernel == 1) {  // v1: operator table read from global memory
+      for (int64_t s = 0; s < nsteps; s++) {
+        k_stage<T, NV, D2, false><<<grid, 32 * wpb, 0, st>>>(u, u, Ua, H->d_nbr, A, nact, ngroups, px, (T)0, c1);
+        k_stage<T, NV, D2, true><<<grid, 32 * wpb, 0, st>>>(Ua, u, Ub, H->d_nbr, A, nact, ngroups, px, a2, c2);
+        k_stage<T, NV, D2, true><<<grid, 32 * wpb, 0, st>>>(Ub, u, u, H->d_nbr, A, nact, ngroups, px, a3, c3);
+      }
+    } else {                 // v2: operator as compile-time immediates, global loads
+      for (int64_t s = 0; s < nsteps; s++) {
+        k_stage_imm<T, NV, P, false><<<grid, 32 * wpb, 0, st>>>(u, u, Ua, H->d_nbr, nact, ngroups, px, (T)0, c1);
+        k_stage_imm<T, NV, P, true><<<grid, 32 * wpb, 0, st>>>(Ua, u, Ub, H->d_nbr, nact, ngroups, px, a2, c2);
+        k_stage_imm<T, NV, P, true><<<grid, 32 * wpb, 0, st>>>(Ub, u, u, H->d_nbr, nact, ngroups, px, a3, c3);
+      }
+    }
+  } else {                   // v3: row-marching bulk-TMA ring (default)
+    (void)A;
+    for (int64_t s = 0; s < nsteps; s++) {
+      CK((launch_ring<T, NV, P, false>(H, u, u, Ua, ngroups, (T)0, c1)));
+      CK((launch_ring<T, NV, P, true>(H, Ua, u, Ub, ngroups, a2, c2)));
+      CK((launch_ring<T, NV, P, true>(H, Ub, u, u, ngroups, a3, c3)));
+    }
+  }
+  if (e1) {
+    CK(cudaEventRecord(e1, st));
+    H->ev_launches_pending += 3 * nsteps;
+  }
+  H->st.launches += 3 * nsteps;
+  H->st.stage_launches += 3 * nsteps;
+  H->st.stage_bytes += 8.0 * pass * nsteps;
+  CK(cudaGetLastError());
+  // K4
+  const int mpx = 256;
+  const int nblk = (nact + mpx - 1) / mpx;
+  size_t need = (size_t)nblk * chunk * 6;
+  if (need > H->partial_cap) {
+    cudaFree(H->d_partial);
+    H->d_partial = nullptr;
+    CK(cudaMalloc(&H->d_partial, need * sizeof(double)));
+    H->partial_cap = need;
+  }
+  dim3 mgrid(nblk, (ngroups + wpb - 1) / wpb);
+  k_moments<T, NV, D2><<<mgrid, 32 * wpb, 0, st>>>(u, H->d_pix, H->d_src_ij, nact, ngroups, mpx, H->d_partial,
+                                               chunk);
+  k_mom_reduce<<<(int)((nvalid + 127) / 128), 128, 0, st>>>(H->d_partial, nblk, chunk, nvalid, H->h, mom_rows);
+  H->st.launches += 2;
+  CK(cudaGetLastError());
+  return DGDIFF_OK;
+}
+
+template <typename T>
+static dgdiff_status run_chunk_p(dgdiff_s *H, int64_t nvalid, int64_t chunk, double dt, int64_t nsteps,
+                                 double *mom_rows) {
+  constexpr int NW = 16 / sizeof(T), NN = 8 / sizeof(T);
+  if (lane_bytes(H) == 16) {
+    if (H->D2 == 6) return run_chunk<T, NW, 6>(H, nvalid, chunk, dt, nsteps, mom_rows);
+    return run_chunk<T, NW, 12>(H, nvalid, chunk, dt, nsteps, mom_rows);
+  }
+  if (H->D2 == 6) return run_chunk<T, NN, 6>(H, nvalid, chunk, dt, nsteps, mom_rows);
+  return run_chunk<T, NN, 12>(H, nvalid, chunk, dt, nsteps, mom_rows);
+}
+
+extern "C" dgdiff_status dgdiff_solve_batch(dgdiff_t H, const int32_t *sources, int64_t n, double dt,
+                                            int64_t nsteps) {
+  if (!H) return fail(DGDIFF_E_ARG, "handle is NULL");
+  if (n < 1 || !sources) return fail(DGDIFF_E_ARG, "need n >= 1 sources");
+  if (n >= (1LL << 31)) return fail(DGDIFF_E_ARG, "too many sources");
+  if (nsteps < 0 || !(dt > 0) || !std::isfinite(dt)) return fail(DGDIFF_E_ARG, "need dt > 0, nsteps >= 0");
+  double dtmax = dgdiff_dt_max(H->p, H->h, H->D);
+  if (dt > dtmax)
+    return fail(DGDIFF_E_UNSTABLE, "dt = %.17g exceeds the SSP-RK3 limit %.17g for P%d", dt, dtmax, H->p);
+  for (int64_t s = 0; s < n; s++) {
+    int i = sources[2 * s], j = sources[2 * s + 1];
+    if (i < 0 || j < 0 || i >= H->nx || j >= H->ny)
+      return fail(DGDIFF_E_SOURCE, "source %lld (%d,%d) is outside the %dx%d grid", (long long)s, i, j, H->nx, H->ny);
+    if (H->h_aidx[(size_t)j * H->nx + i] < 0)
+      return fail(DGDIFF_E_SOURCE, "source %lld (%d,%d) lies on an axon pixel (S:230)", (long long)s, i, j);
+  }
+  CK(cudaSetDevice(H->dev));
+  H->solved = false;
+  H->st.h2d_bytes = 0;
+  H->st.d2h_bytes = 0;
+  int64_t b, e;
+  dgdiff_shard(n, H->o.rank, H->o.nranks, &b, &e);
+  const int64_t nloc = e - b;
+  const int G = gsize(H);
+  // zero-padded moment table for all n sources (K5 all-reduce input)
+  if (n > H->mom_cap) {
+    cudaFree(H->d_mom);
+    H->d_mom = nullptr;
+    CK(cudaMalloc(&H->d_mom, sizeof(double) * 6 * n));
+    H->mom_cap = n;
+  }
+  CK(cudaMemsetAsync(H->d_mom, 0, sizeof(double) * 6 * n, H->stream));
+  if (n > H->src_cap) {
+    cudaFree(H->d_src);
+    H->d_src = nullptr;
+    CK(cudaMalloc(&H->d_src, sizeof(int32_t) * 2 * n));
+    H->src_cap = n;
+  }
+  CK(cudaMemcpyAsync(H->d_src, sources, sizeof(int32_t) * 2 * n, cudaMemcpyHostToDevice, H->stream));
+  H->st.h2d_bytes += sizeof(int32_t) * 2 * n;
+  if (nloc > 0) {
+    // chunk size: fit 3 RK registers in free device memory
+    const size_t per_src = 3 * (size_t)H->nact * H->D2 * tsize(H);
+    int64_t want = (nloc + G - 1) / G * G;
+    int64_t chunk = want;
+    if (H->o.max_chunk > 0) chunk = std::min<int64_t>(chunk, std::max<int64_t>(G, H->o.max_chunk / G * G));
+    if (chunk > H->chunk_cap) {
+      for (int r = 0; r < 3; r++) { cudaFree(H->d_U[r]); H->d_U[r] = nullptr; }
+      cudaFree(H->d_src_a); H->d_src_a = nullptr;
+      cudaFree(H->d_src_ij); H->d_src_ij = nullptr;
+      H->chunk_cap = 0;
+      size_t fr = 0, tot = 0;
+      CK(cudaMemGetInfo(&fr, &tot));
+      int64_t fit = (int64_t)((double)fr * 0.85 / (double)per_src) / G * G;
+      if (fit < G) return fail(DGDIFF_E_NOMEM, "one source group (%d sources) needs %.3g GB", G, per_src * G / 1e9);
+      chunk = std::min(chunk, fit);
+      for (int r = 0; r < 3; r++) CK(cudaMalloc(&H->d_U[r], per_src / 3 * chunk));
+      CK(cudaMalloc(&H->d_src_a, sizeof(int) * chunk));
+      CK(cudaMalloc(&H->d_src_ij, sizeof(int2) * chunk));
+      H->chunk_cap = chunk;
+    } else {
+      chunk = std::min(chunk, H->chunk_cap);
+    }
+    H->st.chunk = chunk;
+    for (int64_t c0 = 0; c0 < nloc; c0 += chunk) {
+      int64_t nvalid = std::min(chunk, nloc - c0);
+      int64_t cpad = (nvalid + G - 1) / G * G;
+      k_src_prep<<<(int)((cpad + 127) / 128), 128, 0, H->stream>>>(H->d_src + 2 * (b + c0), nvalid, cpad,
+                                                                 H->d_aidx, H->nx, H->d_src_a, H->d_src_ij);
+      H->st.launches++;
+      double *rows = H->d_mom + 6 * (b + c0);
+      dgdiff_status s = H->o.precision == 32 ? run_chunk_p<float>(H, nvalid, cpad, dt, nsteps, rows)
+                                             : run_chunk_p<double>(H, nvalid, cpad, dt, nsteps, rows);
+      if (s != DGDIFF_OK) return s;
+      H->last_chunk_begin = b + c0;
+      H->last_chunk_n = nvalid;
+      H->last_chunk_size = cpad;
+    }
+  }
+  H->solved = true;
+  H->last_n = n;
+  H->last_dt = dt;
+  H->last_nsteps = nsteps;
+  return DGDIFF_OK;
+}
+
+extern "C" dgdiff_status dgdiff_covariance(dgdiff_t H, double delta, double sigma[4], double mu[2]) {
+  if (!H) return fail(DGDIFF_E_ARG, "handle is NULL");
+  if (!sigma) return fail(DGDIFF_E_ARG, "sigma is NULL");
+  if (!H->solved) return fail(DGDIFF_E_STATE, "dgdiff_covariance before dgdiff_solve_batch");
+  double t = H->last_nsteps * H->last_dt;
+  if (!(std::fabs(delta - t) <= 1e-12 * std::max(std::fabs(delta), std::fabs(t))))
+    return fail(DGDIFF_E_STATE, "delta = %.17g but the last solve reached nsteps*dt = %.17g", delta, t);
+  CK(cudaSetDevice(H->dev));
+  const int64_t n = H->last_n;
+  if (H->o.nranks > 1) {
+    // the one cross-GPU step: sum of disjoint zero-padded rows is exact
+    ncclResult_t r = g_nccl.allReduce(H->d_mom, H->d_mom, (size_t)6 * n, ncclFloat64, ncclSum, H->comm, H->stream);
+    if (r != ncclSuccess) return fail(DGDIFF_E_NCCL, "ncclAllReduce: %s", g_nccl.errStr(r));
+  }
+  k_finalize<<<1, 256, 0, H->stream>>>(H->d_mom, n, H->o.centering, H->d_out);
+  H->st.launches++;
+  CK(cudaGetLastError());
+  double out[6];
+  CK(cudaMemcpyAsync(out, H->d_out, sizeof out, cudaMemcpyDeviceToHost, H->stream));
+  CK(cudaStreamSynchronize(H->stream));
+  H->st.d2h_bytes += sizeof out;
+  int flags = (int)out[5];
+  if (flags & 2) return fail(DGDIFF_E_NONFINITE, "non-finite moments (unstable run?)");
+  if (flags & 1) return fail(DGDIFF_E_DEGENERATE, "a density has m00 <= 0");
+  sigma[0] = out[0];
+  sigma[1] = out[1];
+  sigma[2] = out[1];
+  sigma[3] = out[2];
+  if (mu) {
+    mu[0] = out[3];
+    mu[1] = out[4];
+  }
+  return DGDIFF_OK;
+}
+
+extern "C" dgdiff_status dgdiff_source_moments(dgdiff_t H, double *out) {
+  if (!H || !out) return fail(DGDIFF_E_ARG, "NULL argument");
+  if (!H->solved) return fail(DGDIFF_E_STATE, "no solve yet");
+  CK(cudaSetDevice(H->dev));
+  CK(cudaMemcpyAsync(out, H->d_mom, sizeof(double) * 6 * H->last_n, cudaMemcpyDeviceToHost, H->stream));
+  CK(cudaStreamSynchronize(H->stream));
+  return DGDIFF_OK;
+}
+
+extern "C" dgdiff_status dgdiff_get_density(dgdiff_t H, int64_t src, double *out) {
+  if (!H || !out) return fail(DGDIFF_E_ARG, "NULL argument");
+  if (!H->solved || !H->o.keep_density) return fail(DGDIFF_E_STATE, "needs keep_density and a solve");
+  if (src < H->last_chunk_begin || src >= H->last_chunk_begin + H->last_chunk_n)
+    return fail(DGDIFF_E_STATE, "source %lld is not in this rank's last chunk [%lld, %lld)", (long long)src,
+                (long long)H->last_chunk_begin, (long long)(H->last_chunk_begin + H->last_chunk_n));
+  CK(cudaSetDevice(H->dev));
+  const int G = gsize(H);
+  int64_t k = src - H->last_chunk_begin;
+  int g = (int)(k / G), slot = (int)(k % G);
+  const int64_t nel = H->nact * H->D2;
+  double *d_tmp = nullptr;
+  CK(cudaMalloc(&d_tmp, sizeof(double) * nel));
+  int blocks = (int)((nel + 255) / 256);
+  const bool wide = lane_bytes(H) == 16;
+  if (H->o.precision == 32) {
+    float *U = (float *)H->d_U[0];
+    if (wide) {
+      if (H->D2 == 6) k_gather<float, 4, 6><<<blocks, 256, 0, H->stream>>>(U, (int)H->nact, g, slot, d_tmp);
+      else k_gather<float, 4, 12><<<blocks, 256, 0, H->stream>>>(U, (int)H->nact, g, slot, d_tmp);
+    } else {
+      if (H->D2 == 6) k_gather<float, 2, 6><<<blocks, 256, 0, H->stream>>>(U, (int)H->nact, g, slot, d_tmp);
+      else k_gather<float, 2, 12><<<blocks, 256, 0, H->stream>>>(U, (int)H->nact, g, slot, d_tmp);
+    }
+  } else {
+    double *U = (double *)H->d_U[0];
+    if (wide) {
+      if (H->D2 == 6) k_gather<double, 2, 6><<<blocks, 256, 0, H->stream>>>(U, (int)H->nact, g, slot, d_tmp);
+      else k_gather<double, 2, 12><<<blocks, 256, 0, H->stream>>>(U, (int)H->nact, g, slot, d_tmp);
+    } else {
+      if (H->D2 == 6) k_gather<double, 1, 6><<<blocks, 256, 0, H->stream>>>(U, (int)H->nact, g, slot, d_tmp);
+      else k_gather<double, 1, 12><<<blocks, 256, 0, H->stream>>>(U, (int)H->nact, g, slot, d_tmp);
+    }
+  }
+  std::vector<double> tmp(nel);
+  cudaError_t e = cudaMemcpyAsync(tmp.data(), d_tmp, sizeof(double) * nel, cudaMemcpyDeviceToHost, H->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(H->stream);
+  cudaFree(d_tmp);
+  if (e != cudaSuccess) return fail(DGDIFF_E_CUDA, "get_density: %s", cudaGetErrorString(e));
+  memset(out, 0, sizeof(double) * (size_t)H->nx * H->ny * H->D2);
+  std::vector<int2> pix(H->nact);
+  CK(cudaMemcpy(pix.data(), H->d_pix, sizeof(int2) * H->nact, cudaMemcpyDeviceToHost));
+  for (int64_t a = 0; a < H->nact; a++)
+    memcpy(out + ((size_t)pix[a].y * H->nx + pix[a].x) * H->D2, tmp.data() + a * H->D2, sizeof(double) * H->D2);
+  return DGDIFF_OK;
+}
+
+extern "C" dgdiff_status dgdiff_set_timing(dgdiff_t H, int32_t enable) {
+  if (!H) return fail(DGDIFF_E_ARG, "handle is NULL");
+  H->timing = enable != 0;
+  return DGDIFF_OK;
+}
+
+extern "C" dgdiff_status dgdiff_reset_stats(dgdiff_t H) {
+  if (!H) return fail(DGDIFF_E_ARG, "handle is NULL");
+  CK(cudaSetDevice(H->dev));
+  CK(cudaStreamSynchronize(H->stream));
+  int64_t na = H->st.n_active, ch = H->st.chunk;
+  memset(&H->st, 0, sizeof H->st);
+  H->st.n_active = na;
+  H->st.chunk = ch;
+  H->ev_used = 0;
+  H->ev_launches_pending = 0;
+  return DGDIFF_OK;
+}
+
+extern "C" dgdiff_status dgdiff_get_stats(dgdiff_t H, dgdiff_stats_t *out) {
+  if (!H || !out) return fail(DGDIFF_E_ARG, "NULL argument");
+  CK(cudaSetDevice(H->dev));
+  if (H->ev_used) {
+    CK(cudaStreamSynchronize(H->stream));
+    double ms = 0;
+    for (size_t k = 0; k < H->ev_used; k++) {
+      float f = 0;
+      CK(cudaEventElapsedTime(&f, H->ev[k].first, H->ev[k].second));
+      ms += f;
+    }
+    H->st.stage_ms += ms;
+    H->ev_used = 0;
+    H->ev_launches_pending = 0;
+  }
+  *out = H->st;
+  return DGDIFF_OK;
+}

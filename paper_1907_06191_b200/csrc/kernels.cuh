@@ -1,0 +1,104 @@
+// kernels.cuh -- shared device helpers of the hot path.
+//
+// State layout: source-minor, extracellular pixels only,
+//   U[g][a][k][G]    g = source group, a = active-pixel index (raster order),
+//                    k = dof slot 0..2d-1 (triangle-major, canonical node
+//                    order), G = 32 lanes x NV sources
+// so one warp owns one pixel x G sources: the open-face code, the operator
+// variant and the masked-pixel skip are warp-uniform, and every access is a
+// coalesced 8- or 16-byte-per-lane load or store.  Axon pixels hold u = 0
+// exactly ("the contribution to the solution is null") and are not
+// stored.  NV = lane bytes / sizeof(T): 16-byte lanes for the global-load
+// kernels (v1, v2), 8-byte lanes for the row-ring kernel (v3), so that a
+// P1 pixel is 1.5 KB and four full row tiles fit in shared memory.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace dgk {
+
+template <typename T, int NV> struct VT;
+template <> struct VT<double, 1> { typedef double type; };
+template <> struct VT<double, 2> { typedef double2 type; };
+template <> struct VT<float, 2> { typedef float2 type; };
+template <> struct VT<float, 4> { typedef float4 type; };
+
+template <typename V, typename T, int NV>
+__device__ __forceinline__ void unpack(const V &v, T (&x)[NV]) {
+  if constexpr (NV == 1) x[0] = v;
+  else if constexpr (NV == 2) { x[0] = v.x; x[1] = v.y; }
+  else { x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w; }
+}
+template <typename V, typename T, int NV>
+__device__ __forceinline__ V pack(const T (&x)[NV]) {
+  V v;
+  if constexpr (NV == 1) v = x[0];
+  else if constexpr (NV == 2) { v.x = x[0]; v.y = x[1]; }
+  else { v.x = x[0]; v.y = x[1]; v.z = x[2]; v.w = x[3]; }
+  return v;
+}
+
+// read-only-path load (state of the previous stage, never written in-kernel)
+template <typename T, int NV>
+__device__ __forceinline__ void ldv(const T *p, T (&x)[NV]) {
+  typedef typename VT<T, NV>::type V;
+  unpack<V, T, NV>(__ldg(reinterpret_cast<const V *>(p)), x);
+}
+// coherent load: u0 may alias the output (stage 3 writes u in place; each
+// element is read and then written by the same thread)
+template <typename T, int NV>
+__device__ __forceinline__ void ldvc(const T *p, T (&x)[NV]) {
+  typedef typename VT<T, NV>::type V;
+  unpack<V, T, NV>(*reinterpret_cast<const V *>(p), x);
+}
+template <typename T, int NV>
+__device__ __forceinline__ void stv(T *p, const T (&x)[NV]) {
+  typedef typename VT<T, NV>::type V;
+  *reinterpret_cast<V *>(p) = pack<V, T, NV>(x);
+}
+// shared-memory load (generic pointer into smem)
+template <typename T, int NV>
+__device__ __forceinline__ void lds(const T *p, T (&x)[NV]) {
+  typedef typename VT<T, NV>::type V;
+  unpack<V, T, NV>(*reinterpret_cast<const V *>(p), x);
+}
+
+__device__ __forceinline__ int open_code(int4 nb) {
+  return (nb.x >= 0) | ((nb.y >= 0) << 1) | ((nb.z >= 0) << 2) | ((nb.w >= 0) << 3);
+}
+
+// ---- mbarrier + 1-D bulk TMA (cp.async.bulk) ---------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+}  // namespace dgk

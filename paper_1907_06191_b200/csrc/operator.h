@@ -1,0 +1,19 @@
+// operator.h -- K0 host precompute (see operator.cpp).
+#pragma once
+#include <vector>
+
+namespace dgop {
+
+struct Table {
+  int p = 0, d = 0;
+  std::vector<double> A;    // [16][5][2d][2d], units D/h^2, exact dyadic
+  std::vector<double> W;    // [2][6][d] moment weights on the unit pixel
+  std::vector<double> init; // [2][d] projected Dirac at the pixel centre, units 1/h^2
+  std::vector<int> nnz;     // [16][5] structural non-zeros per block
+};
+
+// Throws std::runtime_error on failure (unsupported degree, non-dyadic entry,
+// non-zero corner coupling, rational overflow).
+Table build(int p);
+
+}  // namespace dgop

@@ -1,0 +1,219 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle O1,
+element by element on the same seeded inputs, plus the closed forms.
+
+Tolerances (BASELINE.json north_star): fp64 densities <= 1e-12 relative L2,
+Sigma <= 1e-10; fp32 densities <= 1e-5, Sigma <= 1e-4 (relative to the
+diagonal scale, SURVEY §8d "parity norms").
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = {64: dict(dens=1e-12, sig=1e-10, mom=1e-10), 32: dict(dens=1e-5, sig=1e-4, mom=1e-4)}
+
+
+@pytest.fixture(scope="module")
+def dg():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1907_06191_b200 import build
+    build.build_all()
+    from paper_1907_06191_b200 import dgdiff
+    return dgdiff
+
+
+@pytest.fixture(scope="module")
+def cfg():
+    from paper_1907_06191_b200 import configs
+    return configs
+
+
+def rel_l2(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def sig_err(S, R):
+    return np.abs(S - R).max() / max(R[0, 0], R[1, 1])
+
+
+def mom_err(m, r):
+    scale = np.array([1, 1, 1, 1, 1, 1.0]) * np.maximum(np.abs(r[:, :1]), 1e-300)
+    scale[:, 3:] = np.maximum(np.abs(r[:, 3:4]) + np.abs(r[:, 5:6]), 1e-300)
+    scale[:, 1:3] = np.sqrt(scale[:, 3:4])
+    return (np.abs(m - r) / scale).max()
+
+
+@pytest.mark.parametrize("kernel", [0, 1])
+@pytest.mark.parametrize("prec", [64, 32])
+def test_c1_densities_moments_sigma(dg, orc, cfg, prec, kernel):
+    """Config c1 (BASELINE configs[0]): full density parity vs O1."""
+    m = cfg.mask("c1")
+    src = cfg.sources("c1")
+    c = cfg.CONFIGS["c1"]
+    ref_m, ref_d = orc.solve(1, 1.0, 1.0, m, src, c.dt, c.nsteps, keep_density=True)
+    with dg.Solver(m, 1.0, 1.0, 1, precision=prec, keep_density=1, kernel=kernel) as s:
+        s.solve(src, c.dt, c.nsteps)
+        S, mu = s.covariance()
+        got = s.density(0)
+        mom = s.moments()
+    t = TOL[prec]
+    assert rel_l2(got, ref_d[0]) <= t["dens"]
+    assert np.all(got[m.astype(bool)] == 0)                    # axon stasis
+    R, rmu = orc.sigma(ref_m)
+    assert sig_err(S, R) <= t["sig"]
+    assert mom_err(mom, ref_m) <= t["mom"]
+    assert abs(mom[0, 0] - 1) <= (1e-12 if prec == 64 else 2e-6)  # mass
+
+
+@pytest.mark.parametrize("kernel", [0, 1])
+@pytest.mark.parametrize("p,prec", [(1, 64), (1, 32), (2, 64), (2, 32)])
+def test_random_masks_ragged_batches(dg, orc, p, prec, kernel):
+    """Random masks (all 16 face codes, walls at the grid edge), a ragged
+    number of sources (not a multiple of the 64/128-source group), several
+    chunks, P1 and P2."""
+    rng = np.random.default_rng(100 + p * 7 + prec)
+    ny, nx = 23, 29
+    m = (rng.random((ny, nx)) < 0.4).astype(np.uint8)
+    free = np.argwhere(m == 0)
+    G = 64 if prec == 64 else 128                             # sources per warp group
+    n = G + 13                                                # ragged: 2 chunks, 13 in the last
+    pick = free[rng.integers(0, len(free), n)]
+    src = np.stack([pick[:, 1], pick[:, 0]], 1).astype(np.int32)
+    dt = (1 / 32 if p == 1 else 1 / 128) * 0.64 / 1.7         # h = 0.8, D = 1.7
+    nsteps = 60
+    ref_m, ref_d = orc.solve(p, 0.8, 1.7, m, src, dt, nsteps, keep_density=True)
+    with dg.Solver(m, 0.8, 1.7, p, precision=prec, keep_density=1, max_chunk=G, kernel=kernel) as s:
+        s.solve(src, dt, nsteps)
+        S, mu = s.covariance()
+        mom = s.moments()
+        st = s.stats()
+        last = range(G, n)                                    # the last chunk is kept
+        dens = [s.density(k) for k in last]
+    t = TOL[prec]
+    assert st["chunk"] == G
+    for k, dk in zip(last, dens):
+        assert rel_l2(dk, ref_d[k]) <= t["dens"], k
+    R, rmu = orc.sigma(ref_m)
+    assert sig_err(S, R) <= t["sig"]
+    assert np.allclose(mu, rmu, atol=t["sig"] * np.sqrt(R[0, 0]))
+    assert mom_err(mom, ref_m) <= t["mom"]
+
+
+def test_chunking_is_bitwise_invariant(dg, cfg):
+    """Per-source moments do not depend on how sources are chunked, so Sigma
+    is bitwise identical (the property the multi-GPU all-reduce relies on)."""
+    m = cfg.mask("c1")
+    rng = np.random.default_rng(9)
+    free = np.argwhere(m == 0)
+    pick = free[rng.integers(0, len(free), 300)]
+    src = np.stack([pick[:, 1], pick[:, 0]], 1).astype(np.int32)
+    out = []
+    for mc in (0, 64, 128):
+        with dg.Solver(m, 1.0, 1.0, 1, max_chunk=mc) as s:
+            s.solve(src, 1 / 32, 40)
+            out.append((s.covariance()[0], s.moments()))
+    for S, mom in out[1:]:
+        assert np.array_equal(S, out[0][0])
+        assert np.array_equal(mom, out[0][1])
+
+
+@pytest.mark.parametrize("prec", [64, 32])
+def test_c2_free_space_closed_form(dg, orc, cfg, prec):
+    """Config c2 at full size (256^2, 1024 sources, 512 steps): Sigma =
+    2 D Delta I + h^2 [[1/20, 1/15], [1/15, 1/20]] (sharpening
+    P:286-299), and O1 parity on a source subset over 64 steps."""
+    m = cfg.mask("c2")
+    src = cfg.sources("c2")
+    c = cfg.CONFIGS["c2"]
+    with dg.Solver(m, 1.0, 1.0, 1, precision=prec) as s:
+        s.solve(src, c.dt, c.nsteps)
+        S, mu = s.covariance()
+    delta = c.nsteps * c.dt
+    expect = 2 * delta * np.eye(2) + np.array([[1 / 20, 1 / 15], [1 / 15, 1 / 20]])
+    tol = 1e-12 if prec == 64 else 1e-4
+    assert np.abs(S - expect).max() <= tol * expect[0, 0]
+    assert np.abs(mu).max() <= tol * 10
+    sub = src[::128]
+    ref_m, ref_d = orc.solve(1, 1.0, 1.0, m, sub, c.dt, 64, keep_density=True)
+    with dg.Solver(m, 1.0, 1.0, 1, precision=prec, keep_density=1) as s:
+        s.solve(sub, c.dt, 64)
+        for k in range(len(sub)):
+            assert rel_l2(s.density(k), ref_d[k]) <= TOL[prec]["dens"]
+
+
+def test_c2_p2_closed_form(dg, cfg):
+    """P2 variant of c2: Sigma = 2 D Delta I exactly (dt = 1/128, 512 steps)."""
+    m = cfg.mask("c2")
+    src = cfg.sources("c2")[::4]
+    with dg.Solver(m, 1.0, 1.0, 2) as s:
+        s.solve(src, 1 / 128, 512)
+        S, mu = s.covariance()
+    assert np.abs(S - 8.0 * np.eye(2)).max() <= 1e-11 * 8
+
+
+@pytest.mark.parametrize("prec", [64, 32])
+def test_c3_full_batch_sampled_parity(dg, orc, cfg, prec):
+    """Config c3 at full size (512^2 Gamma substrate, 4096 sources, 200 steps)
+    in the bench launch configuration; sampled sources checked one by one
+    against O1 (moments and densities), Sigma of the sample vs O1."""
+    m = cfg.mask("c3")
+    src = cfg.sources("c3")
+    pick = np.array([0, 1337, 2900, 4095])
+    nsteps = 200
+    with dg.Solver(m, 1.0, 1.0, 1, precision=prec, keep_density=1) as s:
+        s.solve(src, 1 / 32, nsteps)
+        S_all, _ = s.covariance()
+        mom = s.moments()
+        dens = {k: s.density(k) for k in pick}
+    ref_m, ref_d = orc.solve(1, 1.0, 1.0, m, src[pick], 1 / 32, nsteps, keep_density=True)
+    t = TOL[prec]
+    for r, k in enumerate(pick):
+        assert rel_l2(dens[k], ref_d[r]) <= t["dens"], k
+    assert mom_err(mom[pick], ref_m) <= t["mom"]
+    S_sub, _ = orc.sigma(ref_m)
+    from oracle import oracle as O
+    S_gpu_sub, _ = O.sigma(mom[pick])     # same finalize on the GPU moments
+    assert sig_err(S_gpu_sub, S_sub) <= t["sig"]
+    # whole-batch properties: mass, symmetry, hindrance
+    assert np.abs(mom[:, 0] - 1).max() <= (1e-12 if prec == 64 else 2e-6)
+    assert S_all[0, 1] == S_all[1, 0]
+    assert S_all[0, 0] < 2 * nsteps / 32 and S_all[1, 1] < 2 * nsteps / 32
+    assert np.linalg.eigvalsh(S_all).min() > 0
+
+
+def test_c4_full_size_sampled_parity(dg, orc, cfg):
+    """Config c4 substrate (2048^2), the bench chunk of 256 sources, sampled
+    against O1 over 8 steps (the oracle needs ~10 s per source-step here)."""
+    m = cfg.mask("c4")
+    src = cfg.sources("c4", 256)
+    pick = np.array([3, 200])
+    with dg.Solver(m, 1.0, 1.0, 1, keep_density=1) as s:
+        s.solve(src, 1 / 32, 8)
+        mom = s.moments()
+        dens = {k: s.density(k) for k in pick}
+    ref_m, ref_d = orc.solve(1, 1.0, 1.0, m, src[pick], 1 / 32, 8, keep_density=True)
+    for r, k in enumerate(pick):
+        assert rel_l2(dens[k], ref_d[r]) <= 1e-12
+    assert mom_err(mom[pick], ref_m) <= 1e-10
+
+
+def test_errors_on_gpu(dg, cfg):
+    m = cfg.mask("c1")
+    with dg.Solver(m, 1.0, 1.0, 1) as s:
+        with pytest.raises(dg.DGDiffError) as e:
+            s.solve([[16, 16]], 1 / 32, 1)                  # axon pixel
+        assert e.value.status == dg.E_SOURCE
+        with pytest.raises(dg.DGDiffError) as e:
+            s.solve([[4, 16]], 0.05, 1)                      # dt > 2.5127/60
+        assert e.value.status == dg.E_UNSTABLE
+        with pytest.raises(dg.DGDiffError) as e:
+            s.covariance(1.0)                                # no solve yet
+        assert e.value.status == dg.E_STATE
+        s.solve([[4, 16]], 1 / 32, 10)
+        with pytest.raises(dg.DGDiffError) as e:
+            s.covariance(1.0)                                # delta != nsteps dt
+        assert e.value.status == dg.E_STATE
+        S, _ = s.covariance(10 / 32)
+        assert S[0, 1] == S[1, 0]
