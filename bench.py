@@ -35,7 +35,8 @@ NX = NY = 2048
 NSTEPS = 32
 DT = 1.0 / 32
 SRC_PER_GPU = 256
-METRIC = "element-dof updates/s"
+METRIC = "element-dof updates/s and \u03a3 solves/s at 1/2/4/8 B200; % of HBM roofline"
+UNIT = "element-dof updates/s"
 
 
 def workload_cfg(args, n_gpus):
@@ -131,12 +132,12 @@ def oracle_threads():
 
 def cpu_baseline(mask, sources, degree):
     th = oracle_threads()
-    nsteps = 2
+    nsteps = 4
     src = sources[:th]
     t = oracle_sample(mask, src, degree, th, nsteps)
     d = (degree + 1) * (degree + 2) // 2
     work = len(src) * 2 * NX * NY * d * nsteps
-    return {"value": work / t, "unit": METRIC, "cores": th, "kind": "oracle",
+    return {"value": work / t, "unit": UNIT, "cores": th, "kind": "oracle",
             "sample": f"{len(src)} sources x {nsteps} SSP-RK3 steps on the same {NX}x{NY} c4 substrate "
                       f"(O1 fp64, one OpenMP thread per source), {t:.1f} s wall"}
 
@@ -161,13 +162,13 @@ def run_reference(args):
     value = work * len(times) / sum(times)
     sample = (f"per step: {th} sources x {nsteps} SSP-RK3 step on the {NX}x{NY} c4 substrate (O1 fp64, "
               f"{th} OpenMP threads); the GPU arm's step is {SRC_PER_GPU} sources x {NSTEPS} steps")
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "dof-updates/s", "n_gpus": world,
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": workload_cfg(args, world) | {"note": "bounded oracle sample"},
-            "cpu_baseline": {"value": value, "unit": "dof-updates/s", "cores": th, "kind": "oracle",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": th, "kind": "oracle",
                              "sample": sample},
-            "e2e": {"value": value, "unit": "dof-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -253,7 +254,7 @@ def run_ours(args):
         if key in tj:
             traffic = tj[key]
     line = {
-        "metric": METRIC, "value": value, "unit": "dof-updates/s", "n_gpus": world, "steps": args.steps,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64" if args.precision == 64 else "f32", "data": "synthetic",
         "config": workload_cfg(args, world),
@@ -266,7 +267,7 @@ def run_ours(args):
                      "algorithmic_bytes_per_launch": per_launch_bytes,
                      "avg_launch_ms": per_launch_ms,
                      "stage_share_of_step": st["stage_ms"] / dev_ms if dev_ms > 0 else None},
-        "e2e": {"value": e2e, "unit": "dof-updates/s", "h2d_bytes_per_step": st["h2d_bytes"],
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": st["h2d_bytes"],
                 "d2h_bytes_per_step": st["d2h_bytes"],
                 "note": "wall clock around dgdiff_solve_batch(host sources) + dgdiff_covariance(host Sigma)"},
         "gpu_launches": st["launches"],

@@ -378,6 +378,8 @@ static size_t tsize(const dgdiff_s *H) { return H->o.precision == 32 ? 4 : 8; }
 // lane width of the state layout: 16 B for the global-load kernels (v1, v2),
 // 8 B for the row-ring kernel (v3, default) so that four full row tiles fit
 static int lane_bytes(const dgdiff_s *H) { return (H->o.kernel == 1 || H->o.kernel == 2) ? 16 : 8; }
+// kernel 9 = diagnostic: the ring kernel streams its inputs without computing
+// (timing experiments only; results are not meaningful)
 static int gsize(const dgdiff_s *H) { return 32 * lane_bytes(H) / (int)tsize(H); }
 static bool use_ring(const dgdiff_s *H) { return !(H->o.kernel == 1 || H->o.kernel == 2); }
 
@@ -642,8 +644,9 @@ static cudaError_t launch_ring(dgdiff_s *H, const T *Uin, const T *U0, T *Uout, 
   nbands = (ny + band_rows - 1) / band_rows;
   const int nitems = per_band * nbands;
   const int grid = std::min(nitems, H->nsm);
-  k_stage_ring<T, NV, P, ALPHA><<<grid, Gm::W * 32, Gm::SMEM, H->stream>>>(
-      Uin, U0, Uout, H->d_nbr, H->d_rowtab, (int)H->nact, ny, H->nstrips, ngroups, band_rows, nitems, alpha, cs);
+  k_stage_ring<T, NV, P, ALPHA><<<grid, Gm::THREADS, Gm::SMEM, H->stream>>>(
+      Uin, U0, Uout, H->d_nbr, H->d_rowtab, (int)H->nact, ny, H->nstrips, ngroups, band_rows, nitems, alpha, cs,
+      H->o.kernel == 9 ? 1 : 0);
   return cudaGetLastError();
 }
 

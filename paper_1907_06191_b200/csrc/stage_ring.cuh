@@ -1,206 +1,306 @@
-// stage_ring.cuh -- K2 v3: one SSP-RK3 stage, row-marching over a shared-memory
-// byte ring filled by 1-D bulk TMA (cp.async.bulk + mbarrier).
+// stage_ring.cuh -- K2 v3: one SSP-RK3 stage, row-marching through shared
+// memory, fed by 1-D bulk TMA (cp.async.bulk) in a warp-specialised
+// producer/consumer pipeline with full/empty mbarriers.
 //
 // Work item = (column strip s of W pixels, source group g of G = 32 NV
-// sources, band of rows [jb0, jb1)).  Because extracellular pixels are stored
-// in raster order, the pixels of row j with x in [x0-1, x0+W+1) are one
-// contiguous run of the state array for group g: one bulk copy per row
-// ("row tile", rowtab[s][j] = {h0, c0, c1, h1} active-index bounds of the
-// halo'd and computed ranges).  Row tiles enter a byte ring in order; thread 0
-// keeps as many rows in flight as the ring holds (adaptive lookahead: sparse
-// Gamma rows are ~40 % of a full row), so every pixel is read from HBM once
-// per stage (plus the 2-column strip halo and 2 band-halo rows).  Warp w
-// computes the w-th extracellular pixel of row j from rows j-1, j, j+1 in
-// shared memory; u0 (the alpha term) and the neighbour indices of row j+1
-// are prefetched into registers one row ahead; outputs go straight to HBM.
+// sources, band of rows [jb0, jb1)).  Extracellular pixels are stored in
+// raster order, so the pixels of row j with x in [x0-1, x0+W+1) are one
+// contiguous run of group g's state: one bulk copy per row ("row tile";
+// rowtab[s][j] = {h0, c0, c1, h1}: active-index bounds of the halo'd and the
+// computed ranges).
 //
-// Ring invariants (checked by construction): the ring is a circular buffer of
-// NSLOT pixel tiles; a row tile may wrap (two bulk copies, one mbarrier), so
-// no space is wasted.  At iteration j thread 0 may overwrite rows <= j-3 only
-// (their last reader, compute(j-2), finished before the barrier of iteration
-// j-1); NSLOT = 4 full rows, so row j+1 can always be issued; at most Q-2
-// rows are live per mbarrier set.
+//   producer warp            for every row r of every item of this CTA, in
+//       batches of up to 32 rows (one per lane): wait until the ring slots are
+//       released (empty barriers), write the row's metadata, arm full[r] with
+//       the byte count and issue the bulk copies: U_in tile [h0, h1) into
+//       ring 1, and -- for rows that are computed -- the u0 tile [c0, c1)
+//       (alpha stages) into ring 2 and the neighbour indices nbr[c0, c1).
+//   consumer warps           the band's computed pixels, dealt out round-robin
+//       in raster order (warp w: pixels w, w+NC, ...): for a pixel of row j,
+//       wait full[j-1..j+1]; apply the 5-point composite operator with
+//       compile-time immediates (stage_imm.cuh) from shared memory, add the
+//       RK combination with u0 from ring 2, store to HBM; release rows whose
+//       last reader has passed.
+//
+// No CTA-wide barrier: warps drift within the ring, the producer keeps as many
+// rows in flight as the rings hold (adaptive lookahead: Gamma rows are ~40 %
+// full), and every pixel is read from HBM once per stage plus the 2-column
+// strip halo and 2 band-halo rows.  Rings are circular buffers of pixel tiles
+// (a tile copy may wrap: two bulk copies on one barrier); ring 1 holds >= 4
+// full row tiles and ring 2 >= 4 full compute rows, so row j+1 can always be
+// issued while rows j-1 and j are held (no deadlock).
 #pragma once
 #include "kernels.cuh"
 #include "stage_imm.cuh"
 
 namespace dgk {
 
-constexpr int RING_Q = 16;        // row entries (mbarriers)
-constexpr int RING_MAXBAND = 512; // max rows per band (+2 halo) for the rowtab cache
+constexpr int RING_Q = 16;         // row entries (full/empty barrier pairs)
+constexpr int RING_MAXBAND = 256;  // max rows per band (+2 halo rows)
 
-template <int P> struct RingCfg;  // warps per CTA = strip width W
-template <> struct RingCfg<1> { static constexpr int W = 32; };
-template <> struct RingCfg<2> { static constexpr int W = 16; };
+template <int P> struct RingCfg;   // consumer warps = strip width W
+template <> struct RingCfg<1> { static constexpr int W = 16; };
+template <> struct RingCfg<2> { static constexpr int W = 8; };
 
 template <typename T, int NV, int P>
 struct RingGeom {
   static constexpr int G = 32 * NV;
   static constexpr int D2 = (P + 1) * (P + 2);
   static constexpr int W = RingCfg<P>::W;
-  static constexpr int PXB = D2 * G * (int)sizeof(T);             // bytes of one pixel tile
-  static constexpr int NSLOT = 4 * (W + 2);                       // ring capacity in pixel tiles
-  static constexpr int RB = NSLOT * PXB;                          // ring bytes: 4 full rows
-  static constexpr int SMEM = RB + RING_Q * 8 + RING_Q * 16 + (RING_MAXBAND + 2) * 16;
+  static constexpr int PXB = D2 * G * (int)sizeof(T);  // one pixel tile (one group)
+  static constexpr int N1 = 4 * (W + 2);               // ring 1 slots (halo'd U_in rows)
+  static constexpr int N2 = 4 * W;                     // ring 2 slots (u0 rows, nbr)
+  static constexpr int OFF_R2 = N1 * PXB;
+  static constexpr int OFF_NB = OFF_R2 + N2 * PXB;
+  static constexpr int OFF_BAR = OFF_NB + N2 * 16;
+  static constexpr int OFF_META = OFF_BAR + 2 * RING_Q * 8;
+  static constexpr int OFF_RT = OFF_META + RING_Q * 32;
+  static constexpr int SMEM = OFF_RT + (RING_MAXBAND + 2) * 16 + 2 * RING_Q * 4;
+  static constexpr int THREADS = (W + 1) * 32;
+  static_assert(SMEM <= 232448, "ring does not fit in shared memory");
 };
 
+struct RowMeta {
+  int p1, h0, c0, c1;   // ring-1 slot of tile start, active-index bounds
+  int p2, pad0, pad1, pad2;
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 template <typename T, int NV, int P, bool HAS_ALPHA>
-__global__ void __launch_bounds__(RingCfg<P>::W * 32, 1)
+__global__ void __launch_bounds__(RingGeom<T, NV, P>::THREADS, 1)
     k_stage_ring(const T *__restrict__ Uin, const T *U0, T *Uout, const int4 *__restrict__ nbr,
                  const int4 *__restrict__ rowtab, int nact, int ny, int nstrips, int ngroups, int band_rows,
-                 int nitems, T alpha, T cs) {
+                 int nitems, T alpha, T cs, int diag) {
   using Gm = RingGeom<T, NV, P>;
-  constexpr int G = Gm::G, D2 = Gm::D2, PXB = Gm::PXB, RB = Gm::RB, Q = RING_Q;
+  constexpr int G = Gm::G, D2 = Gm::D2, PXB = Gm::PXB, Q = RING_Q, W = Gm::W;
   extern __shared__ __align__(128) unsigned char smem[];
-  unsigned char *ring = smem;
-  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + RB);
-  int4 *meta = reinterpret_cast<int4 *>(smem + RB + Q * 8);          // {phys off, h0, -, -}
-  int4 *rt = reinterpret_cast<int4 *>(smem + RB + Q * 8 + Q * 16);   // band rowtab cache
+  unsigned char *ring1 = smem;
+  unsigned char *ring2 = smem + Gm::OFF_R2;
+  int4 *nbr_ring = reinterpret_cast<int4 *>(smem + Gm::OFF_NB);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + Gm::OFF_BAR);
+  uint64_t *empty = full + Q;
+  RowMeta *meta = reinterpret_cast<RowMeta *>(smem + Gm::OFF_META);
+  int4 *rt = reinterpret_cast<int4 *>(smem + Gm::OFF_RT);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) {
-    for (int q = 0; q < Q; q++) mbar_init(&bars[q], 1);
+    for (int q = 0; q < Q; q++) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], W);
+    }
     fence_mbar_init();
   }
   __syncthreads();
-  uint32_t Lbase = 0;               // loads issued by this CTA before the current item
-  uint32_t vst[Q];                  // thread 0: virtual start offset per entry
+  const size_t gstride = (size_t)nact * D2 * G;
+
+  if (w == W) {
+    // =========================== producer warp ===========================
+    // Rows are issued in batches of up to 32, one row per lane: a warp scan
+    // gives every row its ring offsets, the longest prefix that fits is
+    // issued at once (each lane arms its row's barrier and issues its own
+    // bulk copies), and releases are awaited in row order only when the
+    // rings are full.  rv1/rv2[q] = virtual end of the row in entry q.
+    uint32_t *rv = reinterpret_cast<uint32_t *>(rt + RING_MAXBAND + 2);   // [2][Q]
+    uint32_t L = 0;                 // row loads issued by this CTA
+    uint32_t v1 = 0, v2 = 0;        // virtual slot counters of rings 1 and 2
+    uint32_t rel = 0;               // rows whose release has been observed
+    for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+      const int s = item % nstrips;
+      const int g = (item / nstrips) % ngroups;
+      const int b = item / (nstrips * ngroups);
+      const int jb0 = b * band_rows, jb1 = min(ny, jb0 + band_rows);
+      const int lo = max(0, jb0 - 1), hi = min(ny - 1, jb1);
+      __syncwarp();
+      for (int r = lo + lane; r <= hi; r += 32) rt[r - lo] = __ldg(&rowtab[(size_t)s * ny + r]);
+      __syncwarp();
+      const T *Ug = Uin + g * gstride;
+      const T *U0g = U0 + g * gstride;
+      for (int r0 = lo; r0 <= hi;) {
+        const int r = r0 + lane;
+        const bool valid = r <= hi;
+        int4 t = make_int4(0, 0, 0, 0);
+        if (valid) t = rt[r - lo];
+        const bool comp = valid && r >= jb0 && r < jb1;
+        const uint32_t n1 = valid ? (uint32_t)(t.w - t.x) : 0u;
+        const uint32_t n2 = comp ? (uint32_t)(t.z - t.y) : 0u;
+        uint32_t e1 = n1, e2 = n2;                      // inclusive scans
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y1 = __shfl_up_sync(0xffffffffu, e1, o), y2 = __shfl_up_sync(0xffffffffu, e2, o);
+          if (lane >= o) { e1 += y1; e2 += y2; }
+        }
+        const uint32_t nvalid = (uint32_t)min(32, hi - r0 + 1);
+        // wait (in row order) until at least the first row fits, then take
+        // the longest prefix that fits
+        uint32_t take;
+        for (;;) {
+          const uint32_t s1 = rel ? rv[(rel - 1) % Q] : 0u, s2 = rel ? rv[Q + (rel - 1) % Q] : 0u;
+          // L + lane - rel < Q - 1: entry (rel-1) % Q (the live start) is never reused early
+          const bool fits = valid && (L + lane - rel < (uint32_t)(Q - 1)) && (v1 + e1 - s1 <= (uint32_t)Gm::N1) &&
+                            (v2 + e2 - s2 <= (uint32_t)Gm::N2);
+          const uint32_t ok = __ballot_sync(0xffffffffu, fits);
+          take = __ffs(~ok) - 1;                         // length of the fitting prefix
+          if (ok == 0xffffffffu) take = 32;
+          if (take > nvalid) take = nvalid;
+          if (take > 0 || rel == L) break;
+          mbar_wait(&empty[rel % Q], (rel / Q) & 1);
+          rel++;
+        }
+        if (take == 0) take = 1;                         // rel == L: the ring is empty
+        if ((uint32_t)lane < take) {
+          const uint32_t Lr = L + lane, q = Lr % Q;
+          const uint32_t b1 = v1 + e1 - n1, b2 = v2 + e2 - n2;   // virtual starts
+          const uint32_t p1 = b1 % Gm::N1, p2 = b2 % Gm::N2;
+          RowMeta m;
+          m.p1 = (int)p1; m.h0 = t.x; m.c0 = t.y; m.c1 = comp ? t.z : t.y; m.p2 = (int)p2;
+          m.pad0 = m.pad1 = m.pad2 = 0;
+          meta[q] = m;
+          rv[q] = v1 + e1;
+          rv[Q + q] = v2 + e2;
+          const uint32_t bytes = n1 * PXB + (HAS_ALPHA ? n2 * PXB : 0u) + n2 * 16u;
+          mbar_expect_tx(&full[q], bytes);
+          if (n1) {
+            const uint32_t a1 = min(n1, (uint32_t)Gm::N1 - p1);
+            const T *src = Ug + (size_t)t.x * D2 * G;
+            bulk_g2s(ring1 + (size_t)p1 * PXB, src, a1 * PXB, &full[q]);
+            if (n1 > a1) bulk_g2s(ring1, src + (size_t)a1 * D2 * G, (n1 - a1) * PXB, &full[q]);
+          }
+          if (n2) {
+            const uint32_t a2 = min(n2, (uint32_t)Gm::N2 - p2);
+            if (HAS_ALPHA) {
+              const T *src = U0g + (size_t)t.y * D2 * G;
+              bulk_g2s(ring2 + (size_t)p2 * PXB, src, a2 * PXB, &full[q]);
+              if (n2 > a2) bulk_g2s(ring2, src + (size_t)a2 * D2 * G, (n2 - a2) * PXB, &full[q]);
+            }
+            bulk_g2s(nbr_ring + p2, nbr + t.y, a2 * 16u, &full[q]);
+            if (n2 > a2) bulk_g2s(nbr_ring, nbr + t.y + a2, (n2 - a2) * 16u, &full[q]);
+          }
+        }
+        // advance by the issued prefix
+        v1 += __shfl_sync(0xffffffffu, e1, take - 1);
+        v2 += __shfl_sync(0xffffffffu, e2, take - 1);
+        L += take;
+        r0 += (int)take;
+        __syncwarp();
+      }
+    }
+    return;
+  }
+
+  // ============================= consumer warps ============================
+  // The band's computed pixels are dealt out flattened across rows: warp w
+  // takes pixels w, w + NC, w + 2 NC, ... in raster order, so on sparse rows
+  // the warps work on several rows at once.  A warp releases row r once its
+  // cursor has passed row r + 1.
+  constexpr int NC = W;
+  uint32_t Lbase = 0;
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-    const int s = item % nstrips;
     const int g = (item / nstrips) % ngroups;
     const int b = item / (nstrips * ngroups);
     const int jb0 = b * band_rows, jb1 = min(ny, jb0 + band_rows);
     const int lo = max(0, jb0 - 1), hi = min(ny - 1, jb1);
-    for (int r = lo + tid; r <= hi; r += blockDim.x) rt[r - lo] = __ldg(&rowtab[(size_t)s * ny + r]);
-    __syncthreads();
-    const T *Ug = Uin + (size_t)g * nact * D2 * G;
-    const T *U0g = U0 + (size_t)g * nact * D2 * G + lane * NV;
-    T *Uog = Uout + (size_t)g * nact * D2 * G + lane * NV;
-    // producer state (thread 0): wv = virtual pixel-slot counter
-    int ld_row = lo;
-    uint32_t wv = 0;
-    // prefetch row jb0
-    int a_n = -1;
-    int4 nb_n = make_int4(-1, -1, -1, -1);
-    T u0_n[D2][NV];
-    {
-      const int4 t = rt[jb0 - lo];
-      if (t.y + w < t.z) {
-        a_n = t.y + w;
-        nb_n = __ldg(&nbr[a_n]);
-        if (HAS_ALPHA)
+    T *Uog = Uout + g * gstride + lane * NV;
+    auto seq = [&](int r) { return Lbase + (uint32_t)(r - lo); };
+    auto wait_row = [&](int r) {
+      if (r >= lo && r <= hi) {
+        const uint32_t L = seq(r);
+        mbar_wait(&full[L % Q], (L / Q) & 1);
+      }
+    };
+    auto tile1 = [&](const RowMeta &m, int idx) -> const T * {
+      int sl = m.p1 + (idx - m.h0);
+      if (sl >= Gm::N1) sl -= Gm::N1;
+      return reinterpret_cast<const T *>(ring1 + (size_t)sl * PXB) + lane * NV;
+    };
+    int j = jb0, rel_next = lo, cum = 0;
+    wait_row(jb0 - 1);
+    wait_row(jb0);
+    wait_row(jb0 + 1);
+    RowMeta mc = meta[seq(j) % Q];
+    for (int f = w;; f += NC) {
+      while (f >= cum + (mc.c1 - mc.c0)) {      // advance the cursor to f's row
+        cum += mc.c1 - mc.c0;
+        if (++j >= jb1) break;
+        // this warp's remaining pixels lie in rows >= j: rows <= j-2 have had
+        // their last reader; release them before waiting for row j+1 (a warp
+        // must never hold old rows while it waits for new ones)
+        if (rel_next <= j - 2) {
+          __syncwarp();
+          if (lane == 0)
+            for (int r = rel_next; r <= j - 2; r++) mbar_arrive(&empty[seq(r) % Q]);
+          rel_next = j - 1;
+        }
+        wait_row(j + 1);
+        mc = meta[seq(j) % Q];
+      }
+      if (j >= jb1) break;
+      if (diag == 1) continue;   // diagnostic: stream through the ring without computing
+      const int a = mc.c0 + (f - cum);
+      int sl2 = mc.p2 + (a - mc.c0);
+      if (sl2 >= Gm::N2) sl2 -= Gm::N2;
+      const int4 nb = nbr_ring[sl2];
+      const T *ps = tile1(mc, a);
+      T xs[D2][NV], acc[D2][NV], xn[D2][NV];
 #pragma unroll
-          for (int k = 0; k < D2; k++) ldvc<T, NV>(U0g + ((size_t)a_n * D2 + k) * G, u0_n[k]);
+      for (int k = 0; k < D2; k++) lds<T, NV>(ps + k * G, xs[k]);
+#pragma unroll
+      for (int k = 0; k < D2; k++)
+#pragma unroll
+        for (int e = 0; e < NV; e++) acc[k][e] = (T)0;
+      mv_imm<T, NV, P, 0>(acc, xs);
+      if (nb.x >= 0) {
+        const T *pn = tile1(mc, nb.x);
+#pragma unroll
+        for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
+        mv_imm<T, NV, P, 1>(acc, xs);
+        mv_imm<T, NV, P, 5>(acc, xn);
+      }
+      if (nb.y >= 0) {
+        const T *pn = tile1(mc, nb.y);
+#pragma unroll
+        for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
+        mv_imm<T, NV, P, 2>(acc, xs);
+        mv_imm<T, NV, P, 6>(acc, xn);
+      }
+      if (nb.z >= 0) {
+        const RowMeta mn = meta[seq(j + 1) % Q];
+        const T *pn = tile1(mn, nb.z);
+#pragma unroll
+        for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
+        mv_imm<T, NV, P, 3>(acc, xs);
+        mv_imm<T, NV, P, 7>(acc, xn);
+      }
+      if (nb.w >= 0) {
+        const RowMeta ms = meta[seq(j - 1) % Q];
+        const T *pn = tile1(ms, nb.w);
+#pragma unroll
+        for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
+        mv_imm<T, NV, P, 4>(acc, xs);
+        mv_imm<T, NV, P, 8>(acc, xn);
+      }
+      const T *pu = reinterpret_cast<const T *>(ring2 + (size_t)sl2 * PXB) + lane * NV;
+      T *out = Uog + (size_t)a * D2 * G;
+#pragma unroll
+      for (int k = 0; k < D2; k++) {
+        T y[NV];
+        if (HAS_ALPHA) {
+          T z[NV];
+          lds<T, NV>(pu + k * G, z);
+#pragma unroll
+          for (int e = 0; e < NV; e++) y[e] = xs[k][e] + alpha * (z[e] - xs[k][e]) + cs * acc[k][e];
+        } else {
+#pragma unroll
+          for (int e = 0; e < NV; e++) y[e] = xs[k][e] + cs * acc[k][e];
+        }
+        stv<T, NV>(out + (size_t)k * G, y);
       }
     }
-    for (int j = jb0; j < jb1; j++) {
-      if (tid == 0) {
-        const int live = max(lo, j - 2);
-        const uint32_t vlive = (ld_row > live) ? vst[(Lbase + (live - lo)) % Q] : wv;
-        bool fenced = false;
-        while (ld_row <= hi && ld_row - live < Q - 2) {
-          const int4 t = rt[ld_row - lo];
-          const uint32_t cnt = (uint32_t)(t.w - t.x);       // pixel tiles in this row
-          if (wv + cnt - vlive > (uint32_t)Gm::NSLOT) break;
-          const uint32_t L = Lbase + (ld_row - lo), q = L % Q;
-          const uint32_t p0 = wv % Gm::NSLOT;
-          meta[q] = make_int4((int)p0, t.x, 0, 0);
-          vst[q] = wv;
-          if (!fenced) { fence_proxy_async(); fenced = true; }
-          mbar_expect_tx(&bars[q], cnt * PXB);
-          const uint32_t c1 = min(cnt, (uint32_t)Gm::NSLOT - p0);
-          const T *src = Ug + (size_t)t.x * D2 * G;
-          if (c1) bulk_g2s(ring + (size_t)p0 * PXB, src, c1 * PXB, &bars[q]);
-          if (cnt > c1) bulk_g2s(ring, src + (size_t)c1 * D2 * G, (cnt - c1) * PXB, &bars[q]);
-          wv += cnt;
-          ld_row++;
-        }
-      }
-      __syncthreads();
-      // rotate the prefetch registers and issue row j+1's
-      const int a = a_n;
-      const int4 nb = nb_n;
-      T u0v[D2][NV];
-      if (HAS_ALPHA)
-#pragma unroll
-        for (int k = 0; k < D2; k++)
-#pragma unroll
-          for (int e = 0; e < NV; e++) u0v[k][e] = u0_n[k][e];
-      a_n = -1;
-      if (j + 1 < jb1) {
-        const int4 t = rt[j + 1 - lo];
-        if (t.y + w < t.z) {
-          a_n = t.y + w;
-          nb_n = __ldg(&nbr[a_n]);
-          if (HAS_ALPHA)
-#pragma unroll
-            for (int k = 0; k < D2; k++) ldvc<T, NV>(U0g + ((size_t)a_n * D2 + k) * G, u0_n[k]);
-        }
-      }
-      // rows j-1, j, j+1 must have landed
-      for (int r = max(lo, j - 1); r <= min(hi, j + 1); r++) {
-        const uint32_t L = Lbase + (r - lo);
-        mbar_wait(&bars[L % Q], (L / Q) & 1);
-      }
-      if (a >= 0) {
-        // pixel tile address in the ring: slot (row start + index in row) mod NSLOT
-        auto tile = [&](const int4 &m, int idx) -> const T * {
-          int sl = m.x + (idx - m.y);
-          if (sl >= Gm::NSLOT) sl -= Gm::NSLOT;
-          return reinterpret_cast<const T *>(ring + (size_t)sl * PXB) + lane * NV;
-        };
-        const int4 mc = meta[(Lbase + (j - lo)) % Q];
-        const T *ps = tile(mc, a);
-        T xs[D2][NV], acc[D2][NV], xn[D2][NV];
-#pragma unroll
-        for (int k = 0; k < D2; k++) lds<T, NV>(ps + k * G, xs[k]);
-#pragma unroll
-        for (int k = 0; k < D2; k++)
-#pragma unroll
-          for (int e = 0; e < NV; e++) acc[k][e] = (T)0;
-        mv_imm<T, NV, P, 0>(acc, xs);
-        if (nb.x >= 0) {
-          const T *pn = tile(mc, nb.x);
-#pragma unroll
-          for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
-          mv_imm<T, NV, P, 1>(acc, xs);
-          mv_imm<T, NV, P, 5>(acc, xn);
-        }
-        if (nb.y >= 0) {
-          const T *pn = tile(mc, nb.y);
-#pragma unroll
-          for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
-          mv_imm<T, NV, P, 2>(acc, xs);
-          mv_imm<T, NV, P, 6>(acc, xn);
-        }
-        if (nb.z >= 0) {
-          const int4 mn = meta[(Lbase + (j + 1 - lo)) % Q];
-          const T *pn = tile(mn, nb.z);
-#pragma unroll
-          for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
-          mv_imm<T, NV, P, 3>(acc, xs);
-          mv_imm<T, NV, P, 7>(acc, xn);
-        }
-        if (nb.w >= 0) {
-          const int4 ms = meta[(Lbase + (j - 1 - lo)) % Q];
-          const T *pn = tile(ms, nb.w);
-#pragma unroll
-          for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
-          mv_imm<T, NV, P, 4>(acc, xs);
-          mv_imm<T, NV, P, 8>(acc, xn);
-        }
-        T *out = Uog + (size_t)a * D2 * G;
-#pragma unroll
-        for (int k = 0; k < D2; k++) {
-          T y[NV];
-#pragma unroll
-          for (int e = 0; e < NV; e++)
-            y[e] = HAS_ALPHA ? xs[k][e] + alpha * (u0v[k][e] - xs[k][e]) + cs * acc[k][e]
-                             : xs[k][e] + cs * acc[k][e];
-          stv<T, NV>(out + (size_t)k * G, y);
-        }
-      }
-    }
-    __syncthreads();  // item done: ring, rt cache and barriers quiescent
+    // release every row of the item not yet released by this warp
+    __syncwarp();
+    if (lane == 0)
+      for (int r = rel_next; r <= hi; r++) mbar_arrive(&empty[seq(r) % Q]);
     Lbase += (uint32_t)(hi - lo + 1);
   }
 }
