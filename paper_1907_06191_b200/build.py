@@ -18,8 +18,11 @@ LIB = os.path.join(HERE, "libdgdiff.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-SOURCES = ["dgdiff.cu", "operator.cpp"]
-HEADERS = ["kernels.cuh", "operator.h", "stage_imm.cuh", "stage_tb.cuh", "stage_ring.cuh"]
+SOURCES = ["dgdiff.cu", "launch.cu", "stage_v12_f64.cu", "stage_v12_f32.cu", "stage_ring_p1_f64.cu",
+           "stage_ring_p1_f32.cu", "stage_ring_p2_f64.cu", "stage_ring_p2_f32.cu", "operator.cpp"]
+HEADERS = ["kernels.cuh", "operator.h", "stage_imm.cuh", "stage_ring.cuh", "stage_v12.cuh", "launch.h",
+           "stage_tb.cuh"]
+OBJDIR = os.path.join(HERE, "build_obj")
 
 
 def _stale(target, deps):
@@ -48,20 +51,43 @@ def build_tables(force=False) -> str:
     return TABLES
 
 
-def build_dgdiff(force=False, verbose=False) -> str:
-    build_tables(force=force)
-    deps = [TABLES] + [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "dgdiff.h"), __file__]
-    if not force and not _stale(LIB, deps):
-        return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-DDGDIFF_BUILD",
-           "-Xcompiler", "-fPIC,-Wno-free-nonheap-object", "-shared", "-cudart", "static",
-           "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-           "-o", tmp] + [os.path.join(CSRC, f) for f in SOURCES] + ["-ldl"]
+def _compile(src, verbose):
+    """nvcc -c one translation unit (skipped when its object is fresh)."""
+    os.makedirs(OBJDIR, exist_ok=True)
+    obj = os.path.join(OBJDIR, os.path.basename(src) + ".o")
+    deps = [src, TABLES] + [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "dgdiff.h")]
+    if not _stale(obj, deps):
+        return obj
+    tmp = obj + f".tmp{os.getpid()}"
+    cmd = [NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC,-Wno-free-nonheap-object",
+           "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-c", src, "-o", tmp]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.check_call(cmd)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if verbose or r.returncode:
+        sys.stderr.write(r.stdout + r.stderr)
+    if r.returncode:
+        raise subprocess.CalledProcessError(r.returncode, cmd)
+    os.replace(tmp, obj)
+    return obj
+
+
+def build_dgdiff(force=False, verbose=False) -> str:
+    """Compile every TU in parallel (nvcc, sm_100a) and link libdgdiff.so."""
+    from concurrent.futures import ThreadPoolExecutor
+    build_tables(force=force)
+    srcs = [os.path.join(CSRC, f) for f in SOURCES]
+    if force:
+        for f in SOURCES:
+            o = os.path.join(OBJDIR, f + ".o")
+            if os.path.exists(o):
+                os.remove(o)
+    with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(lambda f: _compile(f, verbose), srcs))
+    if not force and not _stale(LIB, objs + [__file__]):
+        return LIB
+    tmp = LIB + f".tmp{os.getpid()}"
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp] + objs + ["-ldl"])
     os.replace(tmp, LIB)
     return LIB
 

@@ -25,8 +25,8 @@
 #include "../../include/dgdiff.h"
 #include "kernels.cuh"
 #include "operator.h"
-#include "stage_imm.cuh"
-#include "stage_ring.cuh"
+#include "launch.h"
+#include "stage_imm.cuh"  // compile-time operator (tab<P>) for the create-time check
 
 using namespace dgk;
 
@@ -81,77 +81,6 @@ __global__ void __launch_bounds__(256) k_init(T *__restrict__ U, int64_t nvec, i
       x[e] = (__ldg(&src_a[s]) == a) ? (T)iv.v[k] : (T)0;
     }
     stv<T, NV>(U + v * NV, x);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// K2: one RK stage,  Uout = Uin + alpha (U0 - Uin) + cs * sum_o A[code][o] Uin[p+o]
-// A in units D/h^2 (exact dyadic); cs = beta dt D/h^2 applied after the sum
-// (SURVEY F4/F9).  One warp = one pixel x G sources; a CTA = WPB source groups
-// of one contiguous range of pixels (pixel index uniform over the CTA).
-// U0 may alias Uout (stage 3 writes u in place: same element, same thread).
-// ---------------------------------------------------------------------------
-template <typename T, int NV, int D2>
-__device__ __forceinline__ void block_mv(T (&acc)[D2][NV], const T *__restrict__ Ab, const T (&x)[D2][NV]) {
-#pragma unroll
-  for (int r = 0; r < D2; r++)
-#pragma unroll
-    for (int c = 0; c < D2; c++) {
-      T a = __ldg(Ab + r * D2 + c);
-#pragma unroll
-      for (int e = 0; e < NV; e++) acc[r][e] = fma(a, x[c][e], acc[r][e]);
-    }
-}
-
-template <typename T, int NV, int D2, bool HAS_ALPHA>
-__global__ void __launch_bounds__(256) k_stage(const T *__restrict__ Uin, const T *U0, T *Uout,
-                                               const int4 *__restrict__ nbr, const T *__restrict__ A,
-                                               int nact, int ngroups, int px_per_cta, T alpha, T cs) {
-  constexpr int G = 32 * NV;
-  const int lane = threadIdx.x & 31;
-  const int g = blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (g >= ngroups) return;
-  const size_t gofs = (size_t)g * nact * D2 * G + lane * NV;
-  const T *Ug = Uin + gofs;
-  const int a0 = blockIdx.x * px_per_cta;
-  const int a1 = min(nact, a0 + px_per_cta);
-  for (int a = a0; a < a1; a++) {
-    const int4 nb = __ldg(&nbr[a]);
-    const int code = open_code(nb);
-    const T *Ac = A + (size_t)code * 5 * D2 * D2;
-    T xs[D2][NV], acc[D2][NV];
-#pragma unroll
-    for (int k = 0; k < D2; k++) ldv<T, NV>(Ug + ((size_t)a * D2 + k) * G, xs[k]);
-#pragma unroll
-    for (int k = 0; k < D2; k++)
-#pragma unroll
-      for (int e = 0; e < NV; e++) acc[k][e] = (T)0;
-    block_mv<T, NV, D2>(acc, Ac, xs);
-    const int nbi[4] = {nb.x, nb.y, nb.z, nb.w};
-#pragma unroll
-    for (int o = 0; o < 4; o++) {
-      if (nbi[o] < 0) continue;  // closed face: neighbour is axon / outside, u+ = 0
-      T xn[D2][NV];
-#pragma unroll
-      for (int k = 0; k < D2; k++) ldv<T, NV>(Ug + ((size_t)nbi[o] * D2 + k) * G, xn[k]);
-      block_mv<T, NV, D2>(acc, Ac + (o + 1) * D2 * D2, xn);
-    }
-    T *out = Uout + gofs + (size_t)a * D2 * G;
-    const T *u0 = U0 + gofs + (size_t)a * D2 * G;
-#pragma unroll
-    for (int k = 0; k < D2; k++) {
-      T y[NV];
-      if (HAS_ALPHA) {
-        T z[NV];
-        ldvc<T, NV>(u0 + (size_t)k * G, z);
-#pragma unroll
-        for (int e = 0; e < NV; e++) y[e] = xs[k][e] + alpha * (z[e] - xs[k][e]) + cs * acc[k][e];
-      } else {
-#pragma unroll
-        for (int e = 0; e < NV; e++) y[e] = xs[k][e] + cs * acc[k][e];
-      }
-      stv<T, NV>(out + (size_t)k * G, y);
-    }
   }
 }
 
@@ -348,6 +277,7 @@ struct dgdiff_s {
   dgop::Table tab;
   // chunk buffers
   void *d_U[3] = {nullptr, nullptr, nullptr};
+  void *d_Ubase = nullptr;
   int64_t chunk_cap = 0;  // sources the U buffers hold
   int *d_src_a = nullptr;
   int2 *d_src_ij = nullptr;
@@ -372,12 +302,22 @@ struct dgdiff_s {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
   size_t ev_used = 0;
   int64_t ev_launches_pending = 0;
+  bool stage_detail = false;          // env DGDIFF_STAGE_DETAIL=1: per-stage events
+  int ahead_alpha = 0, ahead_noalpha = 0;  // env DGDIFF_AHEAD=a,n (tuning experiments)
+  int n1_use = 0, n2_use = 0;              // env DGDIFF_RING=n1,n2 (tuning experiments)
+  double mean_tile = 0;                    // mean ring-kernel row tile (pixel tiles)
+  cudaEvent_t sev[3][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
+  bool sev_pending[3] = {false, false, false};
+  double stage_detail_ms[3] = {0, 0, 0};
 };
 
 static size_t tsize(const dgdiff_s *H) { return H->o.precision == 32 ? 4 : 8; }
 // lane width of the state layout: 16 B for the global-load kernels (v1, v2),
 // 8 B for the row-ring kernel (v3, default) so that four full row tiles fit
-static int lane_bytes(const dgdiff_s *H) { return (H->o.kernel == 1 || H->o.kernel == 2) ? 16 : 8; }
+static int lane_bytes(const dgdiff_s *H) {
+  if (H->o.kernel == 1 || H->o.kernel == 2) return 16;
+  return H->p == 1 ? 16 : 8;  // ring kernel: P1 16-byte lanes, P2 8-byte lanes (tile size)
+}
 // kernel 9 = diagnostic: the ring kernel streams its inputs without computing
 // (timing experiments only; results are not meaningful)
 static int gsize(const dgdiff_s *H) { return 32 * lane_bytes(H) / (int)tsize(H); }
@@ -437,7 +377,10 @@ static void release(dgdiff_s *H) {
     cudaEventDestroy(p.first);
     cudaEventDestroy(p.second);
   }
-  for (int r = 0; r < 3; r++) cudaFree(H->d_U[r]);
+  for (int k = 0; k < 3; k++)
+    for (int e = 0; e < 2; e++)
+      if (H->sev[k][e]) cudaEventDestroy(H->sev[k][e]);
+  cudaFree(H->d_Ubase);
   cudaFree(H->d_nbr);
   cudaFree(H->d_rowtab);
   cudaFree(H->d_pix);
@@ -531,7 +474,7 @@ static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
   }
   // ring kernel row table: active-index bounds of every (strip, row) tile
   if (use_ring(H)) {
-    H->ring_w = H->p == 1 ? RingCfg<1>::W : RingCfg<2>::W;
+    H->ring_w = dgl::ring_width(H->p);
     const int W = H->ring_w;
     H->nstrips = (nx + W - 1) / W;
     std::vector<int> cum((size_t)ny * (nx + 1));
@@ -550,6 +493,12 @@ static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
         auto c = [&](int x) { return cum[(size_t)j * (nx + 1) + std::max(0, std::min(nx, x))]; };
         rtab[(size_t)s * ny + j] = make_int4(c(x0 - 1), c(x0), c(x0 + W), c(x0 + W + 1));
       }
+    // mean halo'd row-tile size (pixel tiles): the ring kernel without the
+    // alpha term keeps ~8 mean rows in flight (measured optimum on c2/c4:
+    // deeper TMA queues delay the row the consumers need next)
+    double tiles = 0;
+    for (const int4 &t : rtab) tiles += t.w - t.x;
+    H->mean_tile = tiles / (double)std::max<size_t>(1, rtab.size());
     CK(cudaMalloc(&H->d_rowtab, sizeof(int4) * rtab.size()));
     CK(cudaMemcpy(H->d_rowtab, rtab.data(), sizeof(int4) * rtab.size(), cudaMemcpyHostToDevice));
   }
@@ -587,6 +536,10 @@ static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
     if (r != ncclSuccess) return fail(DGDIFF_E_NCCL, "ncclCommInitRank: %s", g_nccl.errStr(r));
   }
   H->st.n_active = H->nact;
+  const char *sd = getenv("DGDIFF_STAGE_DETAIL");
+  H->stage_detail = sd && sd[0] == '1';
+  if (const char *ah = getenv("DGDIFF_AHEAD")) sscanf(ah, "%d,%d", &H->ahead_alpha, &H->ahead_noalpha);
+  if (const char *rg = getenv("DGDIFF_RING")) sscanf(rg, "%d,%d", &H->n1_use, &H->n2_use);
   return DGDIFF_OK;
 }
 
@@ -626,30 +579,6 @@ extern "C" dgdiff_status dgdiff_create(dgdiff_t *out, const uint8_t *mask, int32
 // ---------------------------------------------------------------------------
 // solve
 // ---------------------------------------------------------------------------
-template <typename T, int NV, int P, bool ALPHA>
-static cudaError_t launch_ring(dgdiff_s *H, const T *Uin, const T *U0, T *Uout, int ngroups, T alpha, T cs) {
-  using Gm = RingGeom<T, NV, P>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_stage_ring<T, NV, P, ALPHA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Gm::SMEM);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  const int ny = H->ny;
-  const int per_band = H->nstrips * ngroups;
-  int nbands = std::max(1, std::min(ny, (8 * H->nsm + per_band - 1) / per_band));
-  int band_rows = (ny + nbands - 1) / nbands;
-  if (band_rows > RING_MAXBAND) band_rows = RING_MAXBAND;
-  nbands = (ny + band_rows - 1) / band_rows;
-  const int nitems = per_band * nbands;
-  const int grid = std::min(nitems, H->nsm);
-  k_stage_ring<T, NV, P, ALPHA><<<grid, Gm::THREADS, Gm::SMEM, H->stream>>>(
-      Uin, U0, Uout, H->d_nbr, H->d_rowtab, (int)H->nact, ny, H->nstrips, ngroups, band_rows, nitems, alpha, cs,
-      H->o.kernel == 9 ? 1 : 0);
-  return cudaGetLastError();
-}
-
 template <typename T, int NV, int D2>
 static dgdiff_status run_chunk(dgdiff_s *H, int64_t nvalid, int64_t chunk, double dt, int64_t nsteps,
                                double *mom_rows) {
@@ -671,8 +600,6 @@ static dgdiff_status run_chunk(dgdiff_s *H, int64_t nvalid, int64_t chunk, doubl
   const int px = 32;
   dim3 grid((nact + px - 1) / px, (ngroups + wpb - 1) / wpb);
   const double c = dt * H->D / (H->h * H->h);
-  const T a2 = (T)0.75, a3 = (T)(1.0 / 3.0);
-  const T c1 = (T)c, c2 = (T)(0.25 * c), c3 = (T)((2.0 / 3.0) * c);
   const T *A = (const T *)H->d_A;
   const double pass = (double)nact * D2 * chunk * sizeof(T);
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -688,28 +615,56 @@ static dgdiff_status run_chunk(dgdiff_s *H, int64_t nvalid, int64_t chunk, doubl
     H->ev_used++;
     CK(cudaEventRecord(e0, st));
   }
+  // per-stage breakdown (timing mode, first step of the chunk only)
+  auto stage_ev = [&](int k, bool begin) -> dgdiff_status {
+    if (!H->timing || !H->stage_detail) return DGDIFF_OK;
+    if (!H->sev[k][0]) { CK(cudaEventCreate(&H->sev[k][0])); CK(cudaEventCreate(&H->sev[k][1])); }
+    CK(cudaEventRecord(H->sev[k][begin ? 0 : 1], st));
+    if (!begin) H->sev_pending[k] = true;
+    return DGDIFF_OK;
+  };
   constexpr int P = D2 == 6 ? 1 : 2;
-  if constexpr (NV * sizeof(T) == 16) {
-    if (H->o.kernel == 1) {  // v1: operator table read from global memory
-      for (int64_t s = 0; s < nsteps; s++) {
-        k_stage<T, NV, D2, false><<<grid, 32 * wpb, 0, st>>>(u, u, Ua, H->d_nbr, A, nact, ngroups, px, (T)0, c1);
-        k_stage<T, NV, D2, true><<<grid, 32 * wpb, 0, st>>>(Ua, u, Ub, H->d_nbr, A, nact, ngroups, px, a2, c2);
-        k_stage<T, NV, D2, true><<<grid, 32 * wpb, 0, st>>>(Ub, u, u, H->d_nbr, A, nact, ngroups, px, a3, c3);
-      }
-    } else {                 // v2: operator as compile-time immediates, global loads
-      for (int64_t s = 0; s < nsteps; s++) {
-        k_stage_imm<T, NV, P, false><<<grid, 32 * wpb, 0, st>>>(u, u, Ua, H->d_nbr, nact, ngroups, px, (T)0, c1);
-        k_stage_imm<T, NV, P, true><<<grid, 32 * wpb, 0, st>>>(Ua, u, Ub, H->d_nbr, nact, ngroups, px, a2, c2);
-        k_stage_imm<T, NV, P, true><<<grid, 32 * wpb, 0, st>>>(Ub, u, u, H->d_nbr, nact, ngroups, px, a3, c3);
-      }
-    }
-  } else {                   // v3: row-marching bulk-TMA ring (default)
-    (void)A;
-    for (int64_t s = 0; s < nsteps; s++) {
-      CK((launch_ring<T, NV, P, false>(H, u, u, Ua, ngroups, (T)0, c1)));
-      CK((launch_ring<T, NV, P, true>(H, Ua, u, Ub, ngroups, a2, c2)));
-      CK((launch_ring<T, NV, P, true>(H, Ub, u, u, ngroups, a3, c3)));
-    }
+  dgl::StageArgs sa;
+  sa.nbr = H->d_nbr;
+  sa.A = A;
+  sa.rowtab = H->d_rowtab;
+  sa.nact = nact;
+  sa.ny = H->ny;
+  sa.nstrips = H->nstrips;
+  sa.ngroups = ngroups;
+  sa.nsm = H->nsm;
+  sa.px = px;
+  sa.wpb = wpb;
+  sa.diag = H->o.kernel == 9 ? 1 : 0;
+  sa.ahead_alpha = H->ahead_alpha;
+  sa.ahead_noalpha = H->ahead_noalpha;
+  sa.n1_use = H->n1_use > 0 ? H->n1_use : (int)(8.0 * H->mean_tile + 0.5);
+  sa.n2_use = H->n2_use;
+  sa.st = st;
+  const int which = H->o.kernel == 1 ? 0 : H->o.kernel == 2 ? 1 : 2;
+  const int prec = (int)(8 * sizeof(T));
+  auto stage = [&](int k, const T *Uin, T *Uout, double alpha, double cs) -> dgdiff_status {
+    sa.Uin = Uin;
+    sa.U0 = u;
+    sa.Uout = Uout;
+    sa.alpha = alpha;
+    sa.cs = cs;
+    cudaError_t e = dgl::launch_stage(which, prec, P, k > 0, sa);
+    if (e != cudaSuccess) return fail(DGDIFF_E_CUDA, "stage launch: %s", cudaGetErrorString(e));
+    return DGDIFF_OK;
+  };
+  for (int64_t s = 0; s < nsteps; s++) {
+    const bool det = (s == 0);
+    dgdiff_status r;
+    if (det && (r = stage_ev(0, true)) != DGDIFF_OK) return r;
+    if ((r = stage(0, u, Ua, 0.0, c)) != DGDIFF_OK) return r;
+    if (det && (r = stage_ev(0, false)) != DGDIFF_OK) return r;
+    if (det && (r = stage_ev(1, true)) != DGDIFF_OK) return r;
+    if ((r = stage(1, Ua, Ub, 0.75, 0.25 * c)) != DGDIFF_OK) return r;
+    if (det && (r = stage_ev(1, false)) != DGDIFF_OK) return r;
+    if (det && (r = stage_ev(2, true)) != DGDIFF_OK) return r;
+    if ((r = stage(2, Ub, u, 1.0 / 3.0, (2.0 / 3.0) * c)) != DGDIFF_OK) return r;
+    if (det && (r = stage_ev(2, false)) != DGDIFF_OK) return r;
   }
   if (e1) {
     CK(cudaEventRecord(e1, st));
@@ -797,7 +752,9 @@ extern "C" dgdiff_status dgdiff_solve_batch(dgdiff_t H, const int32_t *sources, 
     int64_t chunk = want;
     if (H->o.max_chunk > 0) chunk = std::min<int64_t>(chunk, std::max<int64_t>(G, H->o.max_chunk / G * G));
     if (chunk > H->chunk_cap) {
-      for (int r = 0; r < 3; r++) { cudaFree(H->d_U[r]); H->d_U[r] = nullptr; }
+      cudaFree(H->d_Ubase);
+      H->d_Ubase = nullptr;
+      for (int r = 0; r < 3; r++) H->d_U[r] = nullptr;
       cudaFree(H->d_src_a); H->d_src_a = nullptr;
       cudaFree(H->d_src_ij); H->d_src_ij = nullptr;
       H->chunk_cap = 0;
@@ -806,7 +763,14 @@ extern "C" dgdiff_status dgdiff_solve_batch(dgdiff_t H, const int32_t *sources, 
       int64_t fit = (int64_t)((double)fr * 0.85 / (double)per_src) / G * G;
       if (fit < G) return fail(DGDIFF_E_NOMEM, "one source group (%d sources) needs %.3g GB", G, per_src * G / 1e9);
       chunk = std::min(chunk, fit);
-      for (int r = 0; r < 3; r++) CK(cudaMalloc(&H->d_U[r], per_src / 3 * chunk));
+      // the three RK registers live in one allocation; env DGDIFF_STAGGER=b
+      // offsets register r by r*b extra bytes (layout experiments)
+      {
+        size_t reg = per_src / 3 * chunk, stag = 0;
+        if (const char *e = getenv("DGDIFF_STAGGER")) stag = (size_t)atoll(e) / 256 * 256;
+        CK(cudaMalloc(&H->d_Ubase, 3 * reg + 3 * stag));
+        for (int r = 0; r < 3; r++) H->d_U[r] = (char *)H->d_Ubase + r * (reg + stag);
+      }
       CK(cudaMalloc(&H->d_src_a, sizeof(int) * chunk));
       CK(cudaMalloc(&H->d_src_ij, sizeof(int2) * chunk));
       H->chunk_cap = chunk;
@@ -960,6 +924,16 @@ extern "C" dgdiff_status dgdiff_get_stats(dgdiff_t H, dgdiff_stats_t *out) {
     H->st.stage_ms += ms;
     H->ev_used = 0;
     H->ev_launches_pending = 0;
+  }
+  if (H->stage_detail) {
+    CK(cudaStreamSynchronize(H->stream));
+    for (int k = 0; k < 3; k++)
+      if (H->sev_pending[k]) {
+        float f = 0;
+        CK(cudaEventElapsedTime(&f, H->sev[k][0], H->sev[k][1]));
+        H->sev_pending[k] = false;
+        fprintf(stderr, "[dgdiff] stage %d: %.3f ms\n", k + 1, f);
+      }
   }
   *out = H->st;
   return DGDIFF_OK;

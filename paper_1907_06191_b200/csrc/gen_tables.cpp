@@ -5,7 +5,9 @@
 // exactly as
 //     A[code][self] = V + sum_{f open} F_f,    A[code][f] = N_f  (f open)
 // (checked here entry by entry, in exact arithmetic on the dyadic values).
-// Block ids: 0 = V, 1..4 = F_E, F_W, F_N, F_S, 5..8 = N_E, N_W, N_N, N_S.
+// Block ids: 0 = V, 1..4 = F_E, F_W, F_N, F_S, 5..8 = N_E, N_W, N_N, N_S,
+// 9 + code = the full self block A[code][self] of that open-face code (used
+// by the kernels through a warp-uniform switch: 116 MACs per P1 pixel).
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -18,7 +20,8 @@ static int emit(FILE *f, int p) {
   dgop::Table T = dgop::build(p);
   const int D2 = 2 * T.d;
   auto A = [&](int code, int o, int r, int c) { return T.A[(((size_t)code * 5 + o) * D2 + r) * D2 + c]; };
-  std::vector<double> blk((size_t)9 * D2 * D2, 0.0);
+  const int NB = 9 + 16;
+  std::vector<double> blk((size_t)NB * D2 * D2, 0.0);
   for (int r = 0; r < D2; r++)
     for (int c = 0; c < D2; c++) {
       blk[(0 * D2 + r) * D2 + c] = A(0, 0, r, c);
@@ -26,6 +29,7 @@ static int emit(FILE *f, int p) {
         blk[((1 + fb) * D2 + r) * D2 + c] = A(1 << fb, 0, r, c) - A(0, 0, r, c);
         blk[((5 + fb) * D2 + r) * D2 + c] = A(15, 1 + fb, r, c);
       }
+      for (int code = 0; code < 16; code++) blk[((9 + code) * D2 + r) * D2 + c] = A(code, 0, r, c);
     }
   // verify the decomposition for every code (exact: dyadic values, short mantissas)
   for (int code = 0; code < 16; code++)
@@ -40,10 +44,10 @@ static int emit(FILE *f, int p) {
           if (A(code, 1 + fb, r, c) != want) { fprintf(stderr, "p%d code %d nb %d not fixed\n", p, code, fb); return 1; }
         }
       }
-  fprintf(f, "// P%d: 9 blocks of %dx%d (V, F_E, F_W, F_N, F_S, N_E, N_W, N_N, N_S), units D/h^2\n", p, D2, D2);
+  fprintf(f, "// P%d: blocks of %dx%d (0 V, 1-4 F_E..F_S, 5-8 N_E..N_S, 9+code self[code]), units D/h^2\n", p, D2, D2);
   fprintf(f, "__host__ __device__ constexpr double tab_p%d(int b, int r, int c) {\n  switch ((b * %d + r) * %d + c) {\n", p, D2, D2);
   int nnz = 0;
-  for (int b = 0; b < 9; b++)
+  for (int b = 0; b < NB; b++)
     for (int r = 0; r < D2; r++)
       for (int c = 0; c < D2; c++) {
         double v = blk[((size_t)b * D2 + r) * D2 + c];

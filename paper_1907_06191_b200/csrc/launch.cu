@@ -1,0 +1,16 @@
+// launch.cu -- dispatch of the stage kernels to their translation units
+#include "launch.h"
+#include "stage_ring.cuh"
+
+namespace dgl {
+
+int ring_width(int P) { return P == 1 ? dgk::RingCfg<1, 16>::W : dgk::RingCfg<2, 8>::W; }
+
+cudaError_t launch_stage(int which, int prec, int P, bool alpha, const StageArgs &a) {
+  if (which == 0 || which == 1)
+    return prec == 64 ? launch_v12_f64(which, P, alpha, a) : launch_v12_f32(which, P, alpha, a);
+  if (P == 1) return prec == 64 ? launch_ring_p1_f64(alpha, a) : launch_ring_p1_f32(alpha, a);
+  return prec == 64 ? launch_ring_p2_f64(alpha, a) : launch_ring_p2_f32(alpha, a);
+}
+
+}  // namespace dgl

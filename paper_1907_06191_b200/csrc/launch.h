@@ -1,0 +1,37 @@
+// launch.h -- host-side launchers of the stage kernels (one translation unit
+// per kernel family / precision / degree, compiled in parallel).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace dgl {
+
+struct StageArgs {
+  const void *Uin = nullptr, *U0 = nullptr;  // U0 may alias Uout (stage 3)
+  void *Uout = nullptr;
+  const int4 *nbr = nullptr;
+  const void *A = nullptr;          // v1 only: operator table in global memory
+  const int4 *rowtab = nullptr;     // ring only: [nstrips][ny] {h0, c0, c1, h1}
+  int nact = 0, ny = 0, nstrips = 0, ngroups = 0, nsm = 148;
+  int px = 32, wpb = 4;             // v1/v2 mapping
+  int diag = 0;                     // ring diagnostic (stream without compute)
+  int ahead_alpha = 0, ahead_noalpha = 0;  // ring: max rows in flight (0 = default)
+  int n1_use = 0, n2_use = 0;       // ring: slots used of rings 1 / 2 (0 = all)
+  double alpha = 0, cs = 0;
+  cudaStream_t st = nullptr;
+};
+
+// which: 0 = v1 (table in gmem), 1 = v2 (immediates), 2 = v3 ring (bulk TMA)
+cudaError_t launch_stage(int which, int prec, int P, bool alpha, const StageArgs &a);
+// strip width of the ring kernel for degree P (its row table depends on it)
+int ring_width(int P);
+
+// per-TU entry points
+cudaError_t launch_v12_f64(int which, int P, bool alpha, const StageArgs &a);
+cudaError_t launch_v12_f32(int which, int P, bool alpha, const StageArgs &a);
+cudaError_t launch_ring_p1_f64(bool alpha, const StageArgs &a);
+cudaError_t launch_ring_p1_f32(bool alpha, const StageArgs &a);
+cudaError_t launch_ring_p2_f64(bool alpha, const StageArgs &a);
+cudaError_t launch_ring_p2_f32(bool alpha, const StageArgs &a);
+
+}  // namespace dgl

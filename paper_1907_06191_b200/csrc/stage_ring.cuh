@@ -30,34 +30,49 @@
 // full row tiles and ring 2 >= 4 full compute rows, so row j+1 can always be
 // issued while rows j-1 and j are held (no deadlock).
 #pragma once
+#include <algorithm>
+#include <cstdlib>
 #include "kernels.cuh"
 #include "stage_imm.cuh"
+#include "launch.h"
 
 namespace dgk {
 
 constexpr int RING_Q = 16;         // row entries (full/empty barrier pairs)
+#ifndef RING_N1_NOALPHA            // ring-1 slots without the alpha term
+#define RING_N1_NOALPHA(W, PXB, budget) ((budget) / (PXB))
+#endif
 constexpr int RING_MAXBAND = 256;  // max rows per band (+2 halo rows)
 
-template <int P> struct RingCfg;   // consumer warps = strip width W
-template <> struct RingCfg<1> { static constexpr int W = 16; };
-template <> struct RingCfg<2> { static constexpr int W = 8; };
+// strip width W and consumer warps NC per (degree, lane bytes): a pixel tile is
+// 2d x 32 lanes x lane bytes; four full halo'd rows must fit in ring 1
+template <int P, int LB> struct RingCfg;
+template <> struct RingCfg<1, 8> { static constexpr int W = 16, NC = 16; };
+template <> struct RingCfg<1, 16> { static constexpr int W = 8, NC = 16; };
+template <> struct RingCfg<2, 8> { static constexpr int W = 8, NC = 16; };
 
-template <typename T, int NV, int P>
+template <typename T, int NV, int P, bool ALPHA>
 struct RingGeom {
   static constexpr int G = 32 * NV;
   static constexpr int D2 = (P + 1) * (P + 2);
-  static constexpr int W = RingCfg<P>::W;
+  static constexpr int W = RingCfg<P, NV * (int)sizeof(T)>::W;
+  static constexpr int NC = RingCfg<P, NV * (int)sizeof(T)>::NC;
   static constexpr int PXB = D2 * G * (int)sizeof(T);  // one pixel tile (one group)
-  static constexpr int N1 = 4 * (W + 2);               // ring 1 slots (halo'd U_in rows)
-  static constexpr int N2 = 4 * W;                     // ring 2 slots (u0 rows, nbr)
+  static constexpr int SMEM_MAX = 232448;
+  static constexpr int EXTRA = 2 * RING_Q * 8 + RING_Q * 32 + (RING_MAXBAND + 2) * 16 + 2 * RING_Q * 4;
+  // ring 2 holds u0 tiles (alpha stages) and neighbour indices; without the
+  // alpha term it only holds the 16-byte indices and ring 1 takes the rest
+  static constexpr int N2 = ALPHA ? 4 * W : 16 * W;
+  static constexpr int N1 = ALPHA ? 4 * (W + 2) : RING_N1_NOALPHA(W, PXB, SMEM_MAX - EXTRA - N2 * 16);
   static constexpr int OFF_R2 = N1 * PXB;
-  static constexpr int OFF_NB = OFF_R2 + N2 * PXB;
+  static constexpr int OFF_NB = OFF_R2 + (ALPHA ? N2 * PXB : 0);
   static constexpr int OFF_BAR = OFF_NB + N2 * 16;
   static constexpr int OFF_META = OFF_BAR + 2 * RING_Q * 8;
   static constexpr int OFF_RT = OFF_META + RING_Q * 32;
   static constexpr int SMEM = OFF_RT + (RING_MAXBAND + 2) * 16 + 2 * RING_Q * 4;
-  static constexpr int THREADS = (W + 1) * 32;
-  static_assert(SMEM <= 232448, "ring does not fit in shared memory");
+  static constexpr int THREADS = (NC + 1) * 32;
+  static_assert(SMEM <= SMEM_MAX, "ring does not fit in shared memory");
+  static_assert(N1 >= 4 * (W + 2) && N2 >= 4 * W, "rings too small for progress");
 };
 
 struct RowMeta {
@@ -70,12 +85,12 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 }
 
 template <typename T, int NV, int P, bool HAS_ALPHA>
-__global__ void __launch_bounds__(RingGeom<T, NV, P>::THREADS, 1)
+__global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
     k_stage_ring(const T *__restrict__ Uin, const T *U0, T *Uout, const int4 *__restrict__ nbr,
                  const int4 *__restrict__ rowtab, int nact, int ny, int nstrips, int ngroups, int band_rows,
-                 int nitems, T alpha, T cs, int diag) {
-  using Gm = RingGeom<T, NV, P>;
-  constexpr int G = Gm::G, D2 = Gm::D2, PXB = Gm::PXB, Q = RING_Q, W = Gm::W;
+                 int nitems, T alpha, T cs, int diag, int max_ahead, int n1_use, int n2_use) {
+  using Gm = RingGeom<T, NV, P, HAS_ALPHA>;
+  constexpr int G = Gm::G, D2 = Gm::D2, PXB = Gm::PXB, Q = RING_Q, NC = Gm::NC;
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char *ring1 = smem;
   unsigned char *ring2 = smem + Gm::OFF_R2;
@@ -88,14 +103,14 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P>::THREADS, 1)
   if (tid == 0) {
     for (int q = 0; q < Q; q++) {
       mbar_init(&full[q], 1);
-      mbar_init(&empty[q], W);
+      mbar_init(&empty[q], NC);
     }
     fence_mbar_init();
   }
   __syncthreads();
   const size_t gstride = (size_t)nact * D2 * G;
 
-  if (w == W) {
+  if (w == NC) {
     // =========================== producer warp ===========================
     // Rows are issued in batches of up to 32, one row per lane: a warp scan
     // gives every row its ring offsets, the longest prefix that fits is
@@ -137,9 +152,10 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P>::THREADS, 1)
         uint32_t take;
         for (;;) {
           const uint32_t s1 = rel ? rv[(rel - 1) % Q] : 0u, s2 = rel ? rv[Q + (rel - 1) % Q] : 0u;
-          // L + lane - rel < Q - 1: entry (rel-1) % Q (the live start) is never reused early
-          const bool fits = valid && (L + lane - rel < (uint32_t)(Q - 1)) && (v1 + e1 - s1 <= (uint32_t)Gm::N1) &&
-                            (v2 + e2 - s2 <= (uint32_t)Gm::N2);
+          // L + lane - rel < max_ahead <= Q - 1: rows in flight are capped, and entry
+          // (rel-1) % Q (the live start) is never reused early
+          const bool fits = valid && (L + lane - rel < (uint32_t)max_ahead) && (v1 + e1 - s1 <= (uint32_t)n1_use) &&
+                            (v2 + e2 - s2 <= (uint32_t)n2_use);
           const uint32_t ok = __ballot_sync(0xffffffffu, fits);
           take = __ffs(~ok) - 1;                         // length of the fitting prefix
           if (ok == 0xffffffffu) take = 32;
@@ -194,7 +210,6 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P>::THREADS, 1)
   // takes pixels w, w + NC, w + 2 NC, ... in raster order, so on sparse rows
   // the warps work on several rows at once.  A warp releases row r once its
   // cursor has passed row r + 1.
-  constexpr int NC = W;
   uint32_t Lbase = 0;
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
     const int g = (item / nstrips) % ngroups;
@@ -249,19 +264,19 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P>::THREADS, 1)
       for (int k = 0; k < D2; k++)
 #pragma unroll
         for (int e = 0; e < NV; e++) acc[k][e] = (T)0;
-      mv_imm<T, NV, P, 0>(acc, xs);
+      // self block of this pixel's open-face code (compile-time immediates),
+      // then the fixed neighbour blocks of the open faces
+      mv_self<T, NV, P>(open_code(nb), acc, xs);
       if (nb.x >= 0) {
         const T *pn = tile1(mc, nb.x);
 #pragma unroll
         for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
-        mv_imm<T, NV, P, 1>(acc, xs);
         mv_imm<T, NV, P, 5>(acc, xn);
       }
       if (nb.y >= 0) {
         const T *pn = tile1(mc, nb.y);
 #pragma unroll
         for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
-        mv_imm<T, NV, P, 2>(acc, xs);
         mv_imm<T, NV, P, 6>(acc, xn);
       }
       if (nb.z >= 0) {
@@ -269,7 +284,6 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P>::THREADS, 1)
         const T *pn = tile1(mn, nb.z);
 #pragma unroll
         for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
-        mv_imm<T, NV, P, 3>(acc, xs);
         mv_imm<T, NV, P, 7>(acc, xn);
       }
       if (nb.w >= 0) {
@@ -277,7 +291,6 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P>::THREADS, 1)
         const T *pn = tile1(ms, nb.w);
 #pragma unroll
         for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
-        mv_imm<T, NV, P, 4>(acc, xs);
         mv_imm<T, NV, P, 8>(acc, xn);
       }
       const T *pu = reinterpret_cast<const T *>(ring2 + (size_t)sl2 * PXB) + lane * NV;
@@ -303,6 +316,41 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P>::THREADS, 1)
       for (int r = rel_next; r <= hi; r++) mbar_arrive(&empty[seq(r) % Q]);
     Lbase += (uint32_t)(hi - lo + 1);
   }
+}
+
+// rows in flight per CTA (issued, not yet released): sparse rows stream best
+// with ~8 rows of lookahead, dense rows are limited by ring bytes first
+inline int alpha_max_ahead(const dgl::StageArgs &a, bool alpha) {
+  return alpha ? (a.ahead_alpha > 0 ? a.ahead_alpha : RING_Q - 1) : (a.ahead_noalpha > 0 ? a.ahead_noalpha : RING_Q - 1);
+}
+
+template <typename T, int NV, int P, bool ALPHA>
+cudaError_t launch_ring(const dgl::StageArgs &a) {
+  using Gm = RingGeom<T, NV, P, ALPHA>;
+  static bool attr = false;
+  static int pad = 0;
+  if (!attr) {
+    if (const char *e = getenv("DGDIFF_SMEM_PAD")) pad = atoi(e);
+    if (Gm::SMEM + pad > Gm::SMEM_MAX) pad = Gm::SMEM_MAX - Gm::SMEM;
+    cudaError_t e = cudaFuncSetAttribute(k_stage_ring<T, NV, P, ALPHA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Gm::SMEM + pad);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int per_band = a.nstrips * a.ngroups;
+  int nbands = std::max(1, std::min(a.ny, (8 * a.nsm + per_band - 1) / per_band));
+  int band_rows = (a.ny + nbands - 1) / nbands;
+  if (band_rows > RING_MAXBAND) band_rows = RING_MAXBAND;
+  nbands = (a.ny + band_rows - 1) / band_rows;
+  const int nitems = per_band * nbands;
+  const int grid = std::min(nitems, a.nsm);
+  k_stage_ring<T, NV, P, ALPHA><<<grid, Gm::THREADS, Gm::SMEM + pad, a.st>>>(
+      (const T *)a.Uin, (const T *)a.U0, (T *)a.Uout, a.nbr, a.rowtab, a.nact, a.ny, a.nstrips, a.ngroups,
+      band_rows, nitems, (T)a.alpha, (T)a.cs, a.diag,
+      std::max(4, std::min(RING_Q - 1, alpha_max_ahead(a, ALPHA))),
+      ALPHA ? Gm::N1 : std::max(4 * (Gm::W + 2), std::min(Gm::N1, a.n1_use > 0 ? a.n1_use : Gm::N1)),
+      std::max(4 * Gm::W, std::min(Gm::N2, a.n2_use > 0 ? a.n2_use : Gm::N2)));
+  return cudaGetLastError();
 }
 
 }  // namespace dgk
