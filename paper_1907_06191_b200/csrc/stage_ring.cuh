@@ -48,7 +48,7 @@ constexpr int RING_MAXBAND = 256;  // max rows per band (+2 halo rows)
 // 2d x 32 lanes x lane bytes; four full halo'd rows must fit in ring 1
 template <int P, int LB> struct RingCfg;
 template <> struct RingCfg<1, 8> { static constexpr int W = 16, NC = 16; };
-template <> struct RingCfg<1, 16> { static constexpr int W = 8, NC = 16; };
+template <> struct RingCfg<1, 16> { static constexpr int W = 8, NC = 8; };  // NC swept: 4, 8, 12, 16 -> 8 best
 template <> struct RingCfg<2, 8> { static constexpr int W = 8, NC = 16; };
 
 template <typename T, int NV, int P, bool ALPHA>
