@@ -55,8 +55,10 @@ typedef struct {
                              (P:67-70): not implemented on the GPU path -> E_ARG */
   int32_t centering;      /* 0 = shift each density by its source point (default,
                              reading R12); 1 = by its own mean */
-  int32_t temporal_steps; /* 0 = library choice, 1 = one launch per RK stage,
-                             T_b > 1 = temporal-blocked kernel, T_b steps per pass */
+  int32_t temporal_steps; /* 0 = library choice; 1 = one launch per RK stage
+                             (K2); 2 = fused step (K3: one whole SSP-RK3 step
+                             per launch, temporal blocking over the 3 stages,
+                             degree 1 only -- other degrees use K2) */
   int32_t device;         /* CUDA device ordinal; -1 = current device */
   int32_t rank, nranks;   /* source sharding: rank takes the contiguous block
                              [rank*n/nranks, (rank+1)*n/nranks) of every batch */
@@ -153,6 +155,7 @@ typedef struct {
   double stage_ms;         /* summed device time of those launches (CUDA events on
                               the launch stream), if timing is enabled */
   double stage_bytes;      /* algorithmic HBM bytes of those launches */
+  double stage_flops;      /* algorithmic flops of those launches (structural MACs) */
   int64_t n_active;        /* extracellular pixels */
   int64_t chunk;           /* sources per chunk of the last solve */
   int64_t h2d_bytes, d2h_bytes; /* host<->device bytes moved by the last solve+covariance */

@@ -269,6 +269,9 @@ struct dgdiff_s {
   int64_t nact = 0;
   int4 *d_nbr = nullptr;
   int4 *d_rowtab = nullptr;  // [nstrips][ny] {h0, c0, c1, h1} for the ring kernel
+  int4 *d_rowtab3 = nullptr; // [nstrips3][ny][2] u/U1/U2/output bounds for the fused step
+  int nstrips3 = 0;
+  double macs_per_stage = 0; // structural MACs of one stage over all active pixels (per source)
   int nstrips = 0, ring_w = 0, nsm = 148;
   int2 *d_pix = nullptr;
   int *d_aidx = nullptr;
@@ -314,13 +317,21 @@ struct dgdiff_s {
 static size_t tsize(const dgdiff_s *H) { return H->o.precision == 32 ? 4 : 8; }
 // lane width of the state layout: 16 B for the global-load kernels (v1, v2),
 // 8 B for the row-ring kernel (v3, default) so that four full row tiles fit
-static int lane_bytes(const dgdiff_s *H) {
-  if (H->o.kernel == 1 || H->o.kernel == 2) return 16;
-  return H->p == 1 ? 16 : 8;  // ring kernel: P1 16-byte lanes, P2 8-byte lanes (tile size)
+// K3 (fused step) is used for P1 when temporal_steps == 2 (or by default, see
+// use_fused); its groups are 32 sources (one value per lane)
+static bool use_fused(const dgdiff_s *H) {
+  if (H->p != 1 || H->o.kernel == 1 || H->o.kernel == 2 || H->o.kernel == 9) return false;
+  return H->o.temporal_steps == 2;
 }
-// kernel 9 = diagnostic: the ring kernel streams its inputs without computing
-// (timing experiments only; results are not meaningful)
-static int gsize(const dgdiff_s *H) { return 32 * lane_bytes(H) / (int)tsize(H); }
+// values per lane of the state layout: v1/v2 16-byte lanes; ring P1 16-byte,
+// ring P2 8-byte lanes (tile size); fused step one value per lane
+static int lane_nv(const dgdiff_s *H) {
+  const int ts = (int)tsize(H);
+  if (H->o.kernel == 1 || H->o.kernel == 2) return 16 / ts;
+  if (use_fused(H)) return 1;
+  return (H->p == 1 ? 16 : 8) / ts;
+}
+static int gsize(const dgdiff_s *H) { return 32 * lane_nv(H); }
 static bool use_ring(const dgdiff_s *H) { return !(H->o.kernel == 1 || H->o.kernel == 2); }
 
 extern "C" void dgdiff_opts_default(dgdiff_opts *o) {
@@ -383,6 +394,7 @@ static void release(dgdiff_s *H) {
   cudaFree(H->d_Ubase);
   cudaFree(H->d_nbr);
   cudaFree(H->d_rowtab);
+  cudaFree(H->d_rowtab3);
   cudaFree(H->d_pix);
   cudaFree(H->d_aidx);
   cudaFree(H->d_A);
@@ -502,11 +514,49 @@ static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
     CK(cudaMalloc(&H->d_rowtab, sizeof(int4) * rtab.size()));
     CK(cudaMemcpy(H->d_rowtab, rtab.data(), sizeof(int4) * rtab.size(), cudaMemcpyHostToDevice));
   }
+  // fused-step row table (P1): bounds of the u (3-column halo), U1 (2), U2 (1)
+  // and output ranges of every (strip, row)
+  if (H->p == 1) {
+    const int W = dgl::fused_width(H->o.precision);
+    H->nstrips3 = (nx + W - 1) / W;
+    std::vector<int> cum((size_t)ny * (nx + 1));
+    int run = 0;
+    for (int j = 0; j < ny; j++) {
+      for (int i = 0; i < nx; i++) {
+        cum[(size_t)j * (nx + 1) + i] = run;
+        if (!mask[(size_t)j * nx + i]) run++;
+      }
+      cum[(size_t)j * (nx + 1) + nx] = run;
+    }
+    std::vector<int4> rt3((size_t)H->nstrips3 * ny * 2);
+    for (int s = 0; s < H->nstrips3; s++)
+      for (int j = 0; j < ny; j++) {
+        const int x0 = s * W;
+        auto c = [&](int x) { return cum[(size_t)j * (nx + 1) + std::max(0, std::min(nx, x))]; };
+        rt3[((size_t)s * ny + j) * 2] = make_int4(c(x0 - 3), c(x0 - 2), c(x0 - 1), c(x0));
+        rt3[((size_t)s * ny + j) * 2 + 1] = make_int4(c(x0 + W), c(x0 + W + 1), c(x0 + W + 2), c(x0 + W + 3));
+      }
+    CK(cudaMalloc(&H->d_rowtab3, sizeof(int4) * rt3.size()));
+    CK(cudaMemcpy(H->d_rowtab3, rt3.data(), sizeof(int4) * rt3.size(), cudaMemcpyHostToDevice));
+  }
   H->nsm = prop.multiProcessorCount;
   CK(cudaMalloc(&H->d_nbr, sizeof(int4) * H->nact));
   CK(cudaMalloc(&H->d_pix, sizeof(int2) * H->nact));
   CK(cudaMalloc(&H->d_aidx, sizeof(int) * (size_t)nx * ny));
   CK(cudaMemcpy(H->d_nbr, nbr.data(), sizeof(int4) * H->nact, cudaMemcpyHostToDevice));
+  // algorithmic MACs of one stage (per source): structural non-zeros of the
+  // pixel's self block plus its open neighbour blocks
+  {
+    double macs = 0;
+    for (int64_t a = 0; a < H->nact; a++) {
+      const int4 nb = nbr[a];
+      const int code = (nb.x >= 0) | ((nb.y >= 0) << 1) | ((nb.z >= 0) << 2) | ((nb.w >= 0) << 3);
+      macs += H->tab.nnz[code * 5 + 0];
+      for (int f = 0; f < 4; f++)
+        if ((code >> f) & 1) macs += H->tab.nnz[code * 5 + 1 + f];
+    }
+    H->macs_per_stage = macs;
+  }
   CK(cudaMemcpy(H->d_pix, pix.data(), sizeof(int2) * H->nact, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(H->d_aidx, aidx.data(), sizeof(int) * (size_t)nx * ny, cudaMemcpyHostToDevice));
   // operator table in the state precision (exact: dyadic entries)
@@ -579,6 +629,14 @@ extern "C" dgdiff_status dgdiff_create(dgdiff_t *out, const uint8_t *mask, int32
 // ---------------------------------------------------------------------------
 // solve
 // ---------------------------------------------------------------------------
+// algorithmic flops of one SSP-RK3 step for `chunk` sources: 3 stages of the
+// structural MACs (2 flops each) plus the RK combinations per dof (stage 1:
+// 1 FMA = 2 flops; stages 2, 3: sub + FMA + FMA = 5 flops)
+static double fused_flops_per_step(const dgdiff_s *H, int64_t chunk) {
+  const double dofs = (double)H->nact * H->D2;
+  return (double)chunk * (3.0 * 2.0 * H->macs_per_stage + dofs * (2.0 + 5.0 + 5.0));
+}
+
 template <typename T, int NV, int D2>
 static dgdiff_status run_chunk(dgdiff_s *H, int64_t nvalid, int64_t chunk, double dt, int64_t nsteps,
                                double *mom_rows) {
@@ -653,6 +711,32 @@ static dgdiff_status run_chunk(dgdiff_s *H, int64_t nvalid, int64_t chunk, doubl
     if (e != cudaSuccess) return fail(DGDIFF_E_CUDA, "stage launch: %s", cudaGetErrorString(e));
     return DGDIFF_OK;
   };
+  if (use_fused(H)) {
+    // K3: one fused SSP-RK3 step per launch, ping-pong u <-> Ua
+    sa.rowtab = H->d_rowtab3;
+    sa.nstrips = H->nstrips3;
+    sa.cs = c;
+    T *cur = u, *nxt = Ua;
+    for (int64_t s = 0; s < nsteps; s++) {
+      sa.Uin = cur;
+      sa.U0 = cur;
+      sa.Uout = nxt;
+      cudaError_t e = dgl::launch_step_fused(prec, sa);
+      if (e != cudaSuccess) return fail(DGDIFF_E_CUDA, "fused step launch: %s", cudaGetErrorString(e));
+      std::swap(cur, nxt);
+    }
+    if (cur != u) std::swap(H->d_U[0], H->d_U[1]);   // the final state is always register 0
+    u = (T *)H->d_U[0];
+    if (e1) {
+      CK(cudaEventRecord(e1, st));
+      H->ev_launches_pending += nsteps;
+    }
+    H->st.launches += nsteps;
+    H->st.stage_launches += nsteps;
+    H->st.stage_bytes += 2.0 * pass * nsteps;
+    H->st.stage_flops += fused_flops_per_step(H, chunk) * nsteps;
+    goto after_stepping;
+  }
   for (int64_t s = 0; s < nsteps; s++) {
     const bool det = (s == 0);
     dgdiff_status r;
@@ -673,6 +757,8 @@ static dgdiff_status run_chunk(dgdiff_s *H, int64_t nvalid, int64_t chunk, doubl
   H->st.launches += 3 * nsteps;
   H->st.stage_launches += 3 * nsteps;
   H->st.stage_bytes += 8.0 * pass * nsteps;
+  H->st.stage_flops += fused_flops_per_step(H, chunk) * nsteps;
+after_stepping:
   CK(cudaGetLastError());
   // K4
   const int mpx = 256;
@@ -696,13 +782,20 @@ static dgdiff_status run_chunk(dgdiff_s *H, int64_t nvalid, int64_t chunk, doubl
 template <typename T>
 static dgdiff_status run_chunk_p(dgdiff_s *H, int64_t nvalid, int64_t chunk, double dt, int64_t nsteps,
                                  double *mom_rows) {
-  constexpr int NW = 16 / sizeof(T), NN = 8 / sizeof(T);
-  if (lane_bytes(H) == 16) {
-    if (H->D2 == 6) return run_chunk<T, NW, 6>(H, nvalid, chunk, dt, nsteps, mom_rows);
-    return run_chunk<T, NW, 12>(H, nvalid, chunk, dt, nsteps, mom_rows);
+  const int nv = lane_nv(H);
+  if (nv == 1) {
+    if (H->D2 == 6) return run_chunk<T, 1, 6>(H, nvalid, chunk, dt, nsteps, mom_rows);
+    return run_chunk<T, 1, 12>(H, nvalid, chunk, dt, nsteps, mom_rows);
   }
-  if (H->D2 == 6) return run_chunk<T, NN, 6>(H, nvalid, chunk, dt, nsteps, mom_rows);
-  return run_chunk<T, NN, 12>(H, nvalid, chunk, dt, nsteps, mom_rows);
+  if (nv == 2) {
+    if (H->D2 == 6) return run_chunk<T, 2, 6>(H, nvalid, chunk, dt, nsteps, mom_rows);
+    return run_chunk<T, 2, 12>(H, nvalid, chunk, dt, nsteps, mom_rows);
+  }
+  if constexpr (sizeof(T) == 4) {
+    if (H->D2 == 6) return run_chunk<T, 4, 6>(H, nvalid, chunk, dt, nsteps, mom_rows);
+    return run_chunk<T, 4, 12>(H, nvalid, chunk, dt, nsteps, mom_rows);
+  }
+  return fail(DGDIFF_E_ARG, "internal: lane width");
 }
 
 extern "C" dgdiff_status dgdiff_solve_batch(dgdiff_t H, const int32_t *sources, int64_t n, double dt,
@@ -858,26 +951,16 @@ extern "C" dgdiff_status dgdiff_get_density(dgdiff_t H, int64_t src, double *out
   double *d_tmp = nullptr;
   CK(cudaMalloc(&d_tmp, sizeof(double) * nel));
   int blocks = (int)((nel + 255) / 256);
-  const bool wide = lane_bytes(H) == 16;
+  const int nv = lane_nv(H);
+#define DG_GATHER(TT, NVV)                                                                                     \
+  if (H->D2 == 6) k_gather<TT, NVV, 6><<<blocks, 256, 0, H->stream>>>((TT *)H->d_U[0], (int)H->nact, g, slot, d_tmp); \
+  else k_gather<TT, NVV, 12><<<blocks, 256, 0, H->stream>>>((TT *)H->d_U[0], (int)H->nact, g, slot, d_tmp);
   if (H->o.precision == 32) {
-    float *U = (float *)H->d_U[0];
-    if (wide) {
-      if (H->D2 == 6) k_gather<float, 4, 6><<<blocks, 256, 0, H->stream>>>(U, (int)H->nact, g, slot, d_tmp);
-      else k_gather<float, 4, 12><<<blocks, 256, 0, H->stream>>>(U, (int)H->nact, g, slot, d_tmp);
-    } else {
-      if (H->D2 == 6) k_gather<float, 2, 6><<<blocks, 256, 0, H->stream>>>(U, (int)H->nact, g, slot, d_tmp);
-      else k_gather<float, 2, 12><<<blocks, 256, 0, H->stream>>>(U, (int)H->nact, g, slot, d_tmp);
-    }
+    if (nv == 1) { DG_GATHER(float, 1) } else if (nv == 2) { DG_GATHER(float, 2) } else { DG_GATHER(float, 4) }
   } else {
-    double *U = (double *)H->d_U[0];
-    if (wide) {
-      if (H->D2 == 6) k_gather<double, 2, 6><<<blocks, 256, 0, H->stream>>>(U, (int)H->nact, g, slot, d_tmp);
-      else k_gather<double, 2, 12><<<blocks, 256, 0, H->stream>>>(U, (int)H->nact, g, slot, d_tmp);
-    } else {
-      if (H->D2 == 6) k_gather<double, 1, 6><<<blocks, 256, 0, H->stream>>>(U, (int)H->nact, g, slot, d_tmp);
-      else k_gather<double, 1, 12><<<blocks, 256, 0, H->stream>>>(U, (int)H->nact, g, slot, d_tmp);
-    }
+    if (nv == 1) { DG_GATHER(double, 1) } else { DG_GATHER(double, 2) }
   }
+#undef DG_GATHER
   std::vector<double> tmp(nel);
   cudaError_t e = cudaMemcpyAsync(tmp.data(), d_tmp, sizeof(double) * nel, cudaMemcpyDeviceToHost, H->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(H->stream);

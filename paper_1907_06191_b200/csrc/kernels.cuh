@@ -20,6 +20,7 @@ namespace dgk {
 template <typename T, int NV> struct VT;
 template <> struct VT<double, 1> { typedef double type; };
 template <> struct VT<double, 2> { typedef double2 type; };
+template <> struct VT<float, 1> { typedef float type; };
 template <> struct VT<float, 2> { typedef float2 type; };
 template <> struct VT<float, 4> { typedef float4 type; };
 
@@ -73,6 +74,9 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
 }
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)

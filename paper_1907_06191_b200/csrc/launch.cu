@@ -1,6 +1,7 @@
 // launch.cu -- dispatch of the stage kernels to their translation units
 #include "launch.h"
 #include "stage_ring.cuh"
+#include "step_fused.cuh"
 
 namespace dgl {
 
@@ -11,6 +12,12 @@ cudaError_t launch_stage(int which, int prec, int P, bool alpha, const StageArgs
     return prec == 64 ? launch_v12_f64(which, P, alpha, a) : launch_v12_f32(which, P, alpha, a);
   if (P == 1) return prec == 64 ? launch_ring_p1_f64(alpha, a) : launch_ring_p1_f32(alpha, a);
   return prec == 64 ? launch_ring_p2_f64(alpha, a) : launch_ring_p2_f32(alpha, a);
+}
+
+int fused_width(int prec) { return prec == 64 ? dgk::FusedCfg<double>::W : dgk::FusedCfg<float>::W; }
+
+cudaError_t launch_step_fused(int prec, const StageArgs &a) {
+  return prec == 64 ? launch_fused_f64(a) : launch_fused_f32(a);
 }
 
 }  // namespace dgl

@@ -25,6 +25,11 @@ struct StageArgs {
 cudaError_t launch_stage(int which, int prec, int P, bool alpha, const StageArgs &a);
 // strip width of the ring kernel for degree P (its row table depends on it)
 int ring_width(int P);
+// K3: one fused SSP-RK3 step per pass (P1); a.rowtab = rowtab3 [nstrips][ny][2]
+cudaError_t launch_step_fused(int prec, const StageArgs &a);
+int fused_width(int prec);
+cudaError_t launch_fused_f64(const StageArgs &a);
+cudaError_t launch_fused_f32(const StageArgs &a);
 
 // per-TU entry points
 cudaError_t launch_v12_f64(int which, int P, bool alpha, const StageArgs &a);

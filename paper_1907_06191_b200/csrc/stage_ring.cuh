@@ -80,9 +80,6 @@ struct RowMeta {
   int p2, pad0, pad1, pad2;
 };
 
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 
 template <typename T, int NV, int P, bool HAS_ALPHA>
 __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)

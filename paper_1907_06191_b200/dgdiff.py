@@ -33,7 +33,7 @@ class dgdiff_opts(ctypes.Structure):
 
 class dgdiff_stats_t(ctypes.Structure):
     _fields_ = [("launches", ctypes.c_int64), ("stage_launches", ctypes.c_int64), ("stage_ms", ctypes.c_double),
-                ("stage_bytes", ctypes.c_double), ("n_active", ctypes.c_int64), ("chunk", ctypes.c_int64),
+                ("stage_bytes", ctypes.c_double), ("stage_flops", ctypes.c_double), ("n_active", ctypes.c_int64), ("chunk", ctypes.c_int64),
                 ("h2d_bytes", ctypes.c_int64), ("d2h_bytes", ctypes.c_int64)]
 
 

@@ -217,3 +217,55 @@ def test_errors_on_gpu(dg, cfg):
         assert e.value.status == dg.E_STATE
         S, _ = s.covariance(10 / 32)
         assert S[0, 1] == S[1, 0]
+
+
+# ---------------------------------------------------------------- K3 fused step
+@pytest.mark.parametrize("prec", [64, 32])
+def test_fused_step_c1_and_ragged(dg, orc, cfg, prec):
+    """K3 (one SSP-RK3 step per pass, temporal_steps=2) vs O1: c1 densities and
+    a ragged multi-chunk batch on a random mask (walls, all face codes)."""
+    m = cfg.mask("c1")
+    src = cfg.sources("c1")
+    c = cfg.CONFIGS["c1"]
+    ref_m, ref_d = orc.solve(1, 1.0, 1.0, m, src, c.dt, c.nsteps, keep_density=True)
+    with dg.Solver(m, 1.0, 1.0, 1, precision=prec, keep_density=1, temporal_steps=2) as s:
+        s.solve(src, c.dt, c.nsteps)
+        S, _ = s.covariance()
+        got = s.density(0)
+    t = TOL[prec]
+    assert rel_l2(got, ref_d[0]) <= t["dens"]
+    R, _ = orc.sigma(ref_m)
+    assert sig_err(S, R) <= t["sig"]
+    rng = np.random.default_rng(300 + prec)
+    mk = (rng.random((37, 41)) < 0.4).astype(np.uint8)
+    free = np.argwhere(mk == 0)
+    n = 32 + 9
+    pick = free[rng.integers(0, len(free), n)]
+    srcs = np.stack([pick[:, 1], pick[:, 0]], 1).astype(np.int32)
+    dt = 1 / 32 * 0.49 / 1.3
+    ref_m, ref_d = orc.solve(1, 0.7, 1.3, mk, srcs, dt, 45, keep_density=True)
+    with dg.Solver(mk, 0.7, 1.3, 1, precision=prec, keep_density=1, max_chunk=32, temporal_steps=2) as s:
+        s.solve(srcs, dt, 45)
+        S, _ = s.covariance()
+        mom = s.moments()
+        dens = [s.density(k) for k in range(32, n)]
+    for k, dk in zip(range(32, n), dens):
+        assert rel_l2(dk, ref_d[k]) <= t["dens"], k
+    assert mom_err(mom, ref_m) <= t["mom"]
+    assert sig_err(S, orc.sigma(ref_m)[0]) <= t["sig"]
+
+
+@pytest.mark.parametrize("nsteps", [1, 2, 7])
+def test_fused_step_equals_per_stage(dg, cfg, nsteps):
+    """K3 performs the per-stage kernel's arithmetic in the same order per
+    pixel; on the c3 substrate (several bands and strips) the moments agree to
+    rounding (odd and even step counts exercise the ping-pong buffers)."""
+    m = cfg.mask("c3")
+    src = cfg.sources("c3", 96)
+    out = {}
+    for ts in (1, 2):
+        with dg.Solver(m, 1.0, 1.0, 1, temporal_steps=ts) as s:
+            s.solve(src, 1 / 32, nsteps)
+            out[ts] = (s.moments(), s.covariance()[0])
+    assert mom_err(out[2][0], out[1][0]) <= 1e-13
+    assert np.abs(out[2][1] - out[1][1]).max() <= 1e-13 * out[1][1].max()
