@@ -269,3 +269,23 @@ def test_fused_step_equals_per_stage(dg, cfg, nsteps):
             out[ts] = (s.moments(), s.covariance()[0])
     assert mom_err(out[2][0], out[1][0]) <= 1e-13
     assert np.abs(out[2][1] - out[1][1]).max() <= 1e-13 * out[1][1].max()
+
+
+def test_c5_p2_sampled_parity(dg, orc, cfg):
+    """Config c5 (1024^2 Gamma substrate, P2, dt = 1/128, 64 sources) in its
+    launch configuration, over a 20-step prefix (the oracle needs ~5 s per
+    P2 source-step here); sampled sources vs O1, mass, Sigma symmetric."""
+    m = cfg.mask("c5")
+    src = cfg.sources("c5")
+    pick = np.array([0, 21, 63])
+    with dg.Solver(m, 1.0, 1.0, 2, keep_density=1) as s:
+        s.solve(src, 1 / 128, 20)
+        S, _ = s.covariance()
+        mom = s.moments()
+        dens = {k: s.density(k) for k in pick}
+    ref_m, ref_d = orc.solve(2, 1.0, 1.0, m, src[pick], 1 / 128, 20, keep_density=True)
+    for r, k in enumerate(pick):
+        assert rel_l2(dens[k], ref_d[r]) <= 1e-12, k
+    assert mom_err(mom[pick], ref_m) <= 1e-10
+    assert np.abs(mom[:, 0] - 1).max() <= 1e-12
+    assert S[0, 1] == S[1, 0]
