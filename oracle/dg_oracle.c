@@ -666,3 +666,66 @@ int orc_sigma(const double *mom, int64_t n, int centering, double *sigma, double
     if (!isfinite(sigma[k])) return 4;
   return 0;
 }
+
+/* ------------------------------------------------------------------------- */
+/* Smooth data for convergence tests: L2 projection of the Gaussian          */
+/* g(x) = exp(-|x - x0|^2 / (2 s2)) / (2 pi s2) onto V_h, and the exact L2   */
+/* error of a state against it (free-space solution: s2 -> s2 + 2 D t).      */
+/* ------------------------------------------------------------------------- */
+static double gauss2d(double x, double y, double x0, double y0, double s2) {
+  double r2 = (x - x0) * (x - x0) + (y - y0) * (y - y0);
+  return exp(-0.5 * r2 / s2) / (2.0 * M_PI * s2);
+}
+
+int orc_project_gaussian(int p, double h, int nx, int ny, double x0, double y0, double s2, double *u) {
+  prob_t *P = (prob_t *)malloc(sizeof(prob_t));
+  static const uint8_t dummy = 0;
+  if (setup(P, p, h, 1.0, nx, ny, &dummy, 0) || !(s2 > 0)) { free(P); return 1; }
+  const refel_t *R = &P->R;
+  const int d = R->d;
+  for (int j = 0; j < ny; j++)
+    for (int i = 0; i < nx; i++)
+      for (int t = 0; t < 2; t++) {
+        double b[DMAX] = {0};
+        for (int q = 0; q < R->nq; q++) {
+          double phi[DMAX];
+          basis(p, t, R->qx[t][q][0], R->qx[t][q][1], phi, NULL);
+          double g = gauss2d((i + R->qx[t][q][0]) * h, (j + R->qx[t][q][1]) * h, x0, y0, s2);
+          for (int a = 0; a < d; a++) b[a] += R->qw[t][q] * g * phi[a];
+        }
+        double *uT = u + eidx(P, i, j, t);
+        for (int a = 0; a < d; a++) {
+          double s = 0.0;
+          for (int c = 0; c < d; c++) s += R->Minv[t][a][c] * b[c];
+          uT[a] = s;
+        }
+      }
+  free(P);
+  return 0;
+}
+
+int orc_l2_err_gaussian(int p, double h, int nx, int ny, const double *u, double x0, double y0, double s2,
+                        double *err) {
+  prob_t *P = (prob_t *)malloc(sizeof(prob_t));
+  static const uint8_t dummy = 0;
+  if (setup(P, p, h, 1.0, nx, ny, &dummy, 0) || !(s2 > 0)) { free(P); return 1; }
+  const refel_t *R = &P->R;
+  const int d = R->d;
+  double e2 = 0.0;
+  for (int j = 0; j < ny; j++)
+    for (int i = 0; i < nx; i++)
+      for (int t = 0; t < 2; t++) {
+        const double *uT = u + eidx(P, i, j, t);
+        for (int q = 0; q < R->nq; q++) {
+          double phi[DMAX];
+          basis(p, t, R->qx[t][q][0], R->qx[t][q][1], phi, NULL);
+          double v = 0.0;
+          for (int a = 0; a < d; a++) v += uT[a] * phi[a];
+          double g = gauss2d((i + R->qx[t][q][0]) * h, (j + R->qx[t][q][1]) * h, x0, y0, s2);
+          e2 += R->qw[t][q] * (v - g) * (v - g);
+        }
+      }
+  *err = sqrt(e2);
+  free(P);
+  return 0;
+}

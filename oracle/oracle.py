@@ -52,8 +52,10 @@ def lib():
         L.orc_solve.argtypes = [c_int, c_double, c_double, c_int, c_int, _u8p, c_int, _i32p, c_i64,
                                 c_double, c_i64, _dp, _dp, c_int]
         L.orc_sigma.argtypes = [_dp, c_i64, c_int, _dp, _dp]
+        L.orc_project_gaussian.argtypes = [c_int, c_double, c_int, c_int, c_double, c_double, c_double, _dp]
+        L.orc_l2_err_gaussian.argtypes = [c_int, c_double, c_int, c_int, _dp, c_double, c_double, c_double, _dp]
         for f in (L.orc_reference, L.orc_basis, L.orc_apply_L, L.orc_advance, L.orc_moments,
-                  L.orc_project_delta, L.orc_solve, L.orc_sigma):
+                  L.orc_project_delta, L.orc_solve, L.orc_sigma, L.orc_project_gaussian, L.orc_l2_err_gaussian):
             f.restype = c_int
         _lib = L
     return _lib
@@ -150,3 +152,18 @@ def sigma(mom, centering=0):
     mu = np.zeros(2)
     _chk(lib().orc_sigma(_p(mom), mom.shape[0], centering, _p(s), _p(mu)), "orc_sigma")
     return s.reshape(2, 2), mu
+
+
+def project_gaussian(p, h, nx, ny, x0, y0, s2) -> np.ndarray:
+    """L2 projection of exp(-|x-x0|^2/(2 s2))/(2 pi s2) onto V_h."""
+    u = np.zeros((ny, nx, 2, ndof(p)))
+    _chk(lib().orc_project_gaussian(p, h, nx, ny, x0, y0, s2, _p(u)), "orc_project_gaussian")
+    return u
+
+
+def l2_err_gaussian(p, h, u, x0, y0, s2) -> float:
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    ny, nx = u.shape[:2]
+    e = np.zeros(1)
+    _chk(lib().orc_l2_err_gaussian(p, h, nx, ny, _p(u), x0, y0, s2, _p(e)), "orc_l2_err_gaussian")
+    return float(e[0])
