@@ -74,6 +74,10 @@ typedef struct {
                              by bulk TMA.  Results agree to rounding; the
                              state layout (and so the source-group size) differs:
                              v1/v2 16-byte lanes, v3 8-byte lanes */
+  int32_t mixture_radius; /* R > 0: accumulate the mixture density grid
+                             on the displacement lattice [-R, R]^2 (pixel
+                             units) during dgdiff_solve_batch, for
+                             dgdiff_mixture; 0 (default) = off */
 } dgdiff_opts;
 
 /* Fill *o with the defaults above. */
@@ -111,6 +115,19 @@ dgdiff_status dgdiff_solve_batch(dgdiff_t, const int32_t *sources, int64_t n, do
  * symmetric), mu[2] (nullable) the mixture mean.  Synchronises. */
 dgdiff_status dgdiff_covariance(dgdiff_t, double delta, double sigma[4], double mu[2]);
 
+/* The mixture model u = (1/m) sum_i u_i of the centred, normalised densities
+ * sampled at the displacement nodes (dx, dy) in [-R, R]^2 (pixel
+ * units, R = opts.mixture_radius): u_i(dx, dy) = value of the DG solution of
+ * source i at the centre of pixel (i_s + dx, j_s + dy) (the mean of the two
+ * triangles' traces there; 0 on axon pixels and outside the grid), divided
+ * by its m00; and the least-squares residual of Eq. (9)
+ *   residual = sum_{dx,dy} [ N((dx h, dy h); mu, Sigma) - u(dx, dy) ]^2
+ * with N the Gaussian density of the last dgdiff_covariance.
+ * grid [(2R+1)][(2R+1)] row-major (dy outer), either pointer nullable.
+ * Needs mixture_radius > 0 at create and dgdiff_covariance -> else E_STATE.
+ * When nranks > 1 the grid is all-reduced (NCCL) first.  Synchronises. */
+dgdiff_status dgdiff_mixture(dgdiff_t, double *grid, double *residual);
+
 /* Per-source moments [n][6] = m00 m10 m01 m20 m11 m02 of the last solve,
  * about each source point; rows of other ranks' shards are zero until
  * dgdiff_covariance has run.  Synchronises. */
@@ -145,6 +162,10 @@ void dgdiff_destroy(dgdiff_t);
  *  init [2][d]:  the projected Dirac at the pixel centre times h^2.
  * Any pointer may be NULL. */
 dgdiff_status dgdiff_operator_table(int32_t degree, double *A, double *W, double *init);
+
+/* Values at the pixel centre (1/2, 1/2) of the unit pixel's basis functions,
+ * cw [2][d] (triangle-major, canonical order): the mixture node weights. */
+dgdiff_status dgdiff_centre_weights(int32_t degree, double *cw);
 
 /* Source shard of `rank` out of `nranks` for a batch of n sources. */
 void dgdiff_shard(int64_t n, int32_t rank, int32_t nranks, int64_t *begin, int64_t *end);

@@ -729,3 +729,57 @@ int orc_l2_err_gaussian(int p, double h, int nx, int ny, const double *u, double
   free(P);
   return 0;
 }
+
+/* ------------------------------------------------------------------------- */
+/* The mixture model on the displacement lattice [-R, R]^2 and   */
+/* the least-squares residual of Eq. (9) against the Gaussian   */
+/* density N(x; mu, Sigma) of P:252.  Node value of source s at (dx, dy):    */
+/* the DG solution at the centre of pixel (is+dx, js+dy), taken as the mean  */
+/* of the L and U traces there (the centre lies on their shared diagonal,    */
+/* DESIGN.md reading R20), divided by m00_s ("centering and normalization",  */
+/* P:243).  dens: [n][ny][nx][2][d]; grid: [2R+1][2R+1], dy outer.           */
+/* ------------------------------------------------------------------------- */
+int orc_mixture(int p, int nx, int ny, const double *dens, const int32_t *sources, const double *mom, int64_t n,
+                int R, double *grid) {
+  if (p < 1 || p > 3 || n < 1 || R < 0) return 1;
+  const int d = (p + 1) * (p + 2) / 2, side = 2 * R + 1;
+  double phiL[DMAX], phiU[DMAX];
+  basis(p, 0, 0.5, 0.5, phiL, NULL);
+  basis(p, 1, 0.5, 0.5, phiU, NULL);
+  for (int c = 0; c < side * side; c++) grid[c] = 0.0;
+  for (int64_t s = 0; s < n; s++) {
+    const double *u = dens + (size_t)s * nx * ny * 2 * d;
+    const int is = sources[2 * s], js = sources[2 * s + 1];
+    for (int dy = -R; dy <= R; dy++)
+      for (int dx = -R; dx <= R; dx++) {
+        const int i = is + dx, j = js + dy;
+        if (i < 0 || j < 0 || i >= nx || j >= ny) continue;
+        const double *uL = u + (((size_t)j * nx + i) * 2 + 0) * d;
+        const double *uU = uL + d;
+        double vL = 0.0, vU = 0.0;
+        for (int a = 0; a < d; a++) { vL += uL[a] * phiL[a]; vU += uU[a] * phiU[a]; }
+        grid[(dy + R) * side + (dx + R)] += 0.5 * (vL + vU) / mom[6 * s];
+      }
+  }
+  for (int c = 0; c < side * side; c++) grid[c] /= (double)n;
+  return 0;
+}
+
+int orc_residual(const double *grid, int R, double h, const double *sigma, const double *mu, double *res) {
+  const int side = 2 * R + 1;
+  const double sxx = sigma[0], sxy = sigma[1], syy = sigma[3];
+  const double det = sxx * syy - sxy * sxy;
+  if (!(det > 0)) return 6;
+  double r = 0.0;
+  for (int dy = -R; dy <= R; dy++)
+    for (int dx = -R; dx <= R; dx++) {
+      const double x = dx * h - mu[0], y = dy * h - mu[1];
+      /* (x, y) Sigma^-1 (x, y)^T */
+      const double q = (syy * x * x - 2.0 * sxy * x * y + sxx * y * y) / det;
+      const double g = exp(-0.5 * q) / (2.0 * M_PI * sqrt(det));
+      const double e = g - grid[(dy + R) * side + (dx + R)];
+      r += e * e;
+    }
+  *res = r;
+  return 0;
+}

@@ -52,10 +52,12 @@ def lib():
         L.orc_solve.argtypes = [c_int, c_double, c_double, c_int, c_int, _u8p, c_int, _i32p, c_i64,
                                 c_double, c_i64, _dp, _dp, c_int]
         L.orc_sigma.argtypes = [_dp, c_i64, c_int, _dp, _dp]
+        L.orc_mixture.argtypes = [c_int, c_int, c_int, _dp, _i32p, _dp, c_i64, c_int, _dp]
+        L.orc_residual.argtypes = [_dp, c_int, c_double, _dp, _dp, _dp]
         L.orc_project_gaussian.argtypes = [c_int, c_double, c_int, c_int, c_double, c_double, c_double, _dp]
         L.orc_l2_err_gaussian.argtypes = [c_int, c_double, c_int, c_int, _dp, c_double, c_double, c_double, _dp]
         for f in (L.orc_reference, L.orc_basis, L.orc_apply_L, L.orc_advance, L.orc_moments,
-                  L.orc_project_delta, L.orc_solve, L.orc_sigma, L.orc_project_gaussian, L.orc_l2_err_gaussian):
+                  L.orc_project_delta, L.orc_solve, L.orc_sigma, L.orc_project_gaussian, L.orc_l2_err_gaussian, L.orc_mixture, L.orc_residual):
             f.restype = c_int
         _lib = L
     return _lib
@@ -167,3 +169,25 @@ def l2_err_gaussian(p, h, u, x0, y0, s2) -> float:
     e = np.zeros(1)
     _chk(lib().orc_l2_err_gaussian(p, h, nx, ny, _p(u), x0, y0, s2, _p(e)), "orc_l2_err_gaussian")
     return float(e[0])
+
+
+def mixture(p, dens, sources, mom, R) -> np.ndarray:
+    """Mixture grid [(2R+1)][(2R+1)] of the centred, normalised densities."""
+    dens = np.ascontiguousarray(dens, dtype=np.float64)
+    n, ny, nx = dens.shape[:3]
+    src = np.ascontiguousarray(sources, dtype=np.int32).reshape(-1, 2)
+    mom = np.ascontiguousarray(mom, dtype=np.float64).reshape(-1, 6)
+    g = np.zeros((2 * R + 1, 2 * R + 1))
+    _chk(lib().orc_mixture(p, nx, ny, _p(dens), _p(src, _i32p), _p(mom), n, R, _p(g)), "orc_mixture")
+    return g
+
+
+def residual(grid, h, S, mu) -> float:
+    """Eq. (9): sum over nodes of (N(x; mu, Sigma) - grid)^2."""
+    grid = np.ascontiguousarray(grid, dtype=np.float64)
+    R = (grid.shape[0] - 1) // 2
+    S = np.ascontiguousarray(S, dtype=np.float64).reshape(4)
+    mu = np.ascontiguousarray(mu, dtype=np.float64).reshape(2)
+    r = np.zeros(1)
+    _chk(lib().orc_residual(_p(grid), R, h, _p(S), _p(mu), _p(r)), "orc_residual")
+    return float(r[0])

@@ -56,6 +56,7 @@ static dgdiff_status fail(dgdiff_status s, const char *fmt, ...) {
 // ---------------------------------------------------------------------------
 #define DMAXK 6                    // max dofs per triangle on the GPU path (P2)
 __constant__ double c_W[2 * 6 * DMAXK];    // moment weights (unit pixel)
+__constant__ double c_CW[2 * DMAXK];       // basis values at the pixel centre (mixture nodes)
 
 struct InitVals { double v[2 * DMAXK]; };  // projected Dirac / h^2
 
@@ -232,6 +233,71 @@ __global__ void k_src_prep(const int32_t *__restrict__ src, int64_t nvalid, int6
 }
 
 // ---------------------------------------------------------------------------
+// N2: mixture density grid on the displacement lattice [-R, R]^2.
+// One thread per node (dx, dy) loops over the chunk's sources in order (fixed
+// summation order: deterministic).  Node value of source s: the mean of the L
+// and U traces at the centre of pixel (is+dx, js+dy), divided by m00_s.
+// ---------------------------------------------------------------------------
+template <typename T, int NV, int D2>
+__global__ void k_mixture(const T *__restrict__ U, const int *__restrict__ aidx, int nx, int ny, int nact,
+                          const int2 *__restrict__ src_ij, const double *__restrict__ mom, int64_t nvalid, int R,
+                          double *__restrict__ grid) {
+  constexpr int G = 32 * NV, d = D2 / 2;
+  const int side = 2 * R + 1;
+  const int cell = blockIdx.x * blockDim.x + threadIdx.x;
+  if (cell >= side * side) return;
+  const int dx = cell % side - R, dy = cell / side - R;
+  double acc = 0.0;
+  for (int64_t s = 0; s < nvalid; s++) {
+    const int2 ij = __ldg(&src_ij[s]);
+    const int i = ij.x + dx, j = ij.y + dy;
+    if (i < 0 || j < 0 || i >= nx || j >= ny) continue;
+    const int a = __ldg(&aidx[(size_t)j * nx + i]);
+    if (a < 0) continue;
+    const int64_t g = s / G;
+    const int slot = (int)(s % G);
+    const T *p = U + ((size_t)g * nact + a) * D2 * G + slot;
+    double vl = 0.0, vu = 0.0;
+#pragma unroll
+    for (int k = 0; k < d; k++) {
+      vl += c_CW[k] * (double)p[(size_t)k * G];
+      vu += c_CW[DMAXK + k] * (double)p[(size_t)(d + k) * G];
+    }
+    acc += 0.5 * (vl + vu) / mom[s * 6];
+  }
+  grid[cell] += acc;
+}
+
+// normalise by the source count and evaluate the Eq. (9) residual against the
+// Gaussian N(x; mu, Sigma); one block, fixed-order reduction
+__global__ void __launch_bounds__(256) k_mixture_final(const double *__restrict__ gsum, int R, double h, int64_t n,
+                                                       double sxx, double sxy, double syy, double mx, double my,
+                                                       double *__restrict__ grid_out, double *__restrict__ res_out) {
+  __shared__ double sh[256];
+  const int side = 2 * R + 1, ncell = side * side, t = threadIdx.x;
+  const double det = sxx * syy - sxy * sxy;
+  const double ixx = syy / det, ixy = -sxy / det, iyy = sxx / det;
+  const double norm = 1.0 / (2.0 * M_PI * sqrt(det));
+  const double inv_n = 1.0 / (double)n;
+  const int b = (int)((int64_t)ncell * t / 256), e = (int)((int64_t)ncell * (t + 1) / 256);
+  double r = 0.0;
+  for (int c = b; c < e; c++) {
+    const double v = gsum[c] * inv_n;
+    grid_out[c] = v;
+    const double x = (c % side - R) * h - mx, y = (c / side - R) * h - my;
+    const double gauss = norm * exp(-0.5 * (ixx * x * x + 2.0 * ixy * x * y + iyy * y * y));
+    r += (gauss - v) * (gauss - v);
+  }
+  sh[t] = r;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (t < w) sh[t] += sh[t + w];
+    __syncthreads();
+  }
+  if (t == 0) *res_out = sh[0];
+}
+
+// ---------------------------------------------------------------------------
 // NCCL (dlopen'ed: only needed when nranks > 1)
 // ---------------------------------------------------------------------------
 struct NcclApi {
@@ -291,6 +357,11 @@ struct dgdiff_s {
   double *d_mom = nullptr;
   int64_t mom_cap = 0;
   double *d_out = nullptr;
+  // mixture grid (N2)
+  double *d_mix = nullptr, *d_mix_out = nullptr;
+  int mix_R = 0;
+  bool mix_reduced = false, have_sigma = false;
+  double last_sigma[3] = {0, 0, 0}, last_mu[2] = {0, 0};
   // last solve
   bool solved = false;
   int64_t last_n = 0, last_nsteps = 0;
@@ -349,6 +420,7 @@ extern "C" void dgdiff_opts_default(dgdiff_opts *o) {
   o->max_chunk = 0;
   o->stream = nullptr;
   o->kernel = 0;
+  o->mixture_radius = 0;
 }
 
 extern "C" const char *dgdiff_last_error(void) { return g_err.c_str(); }
@@ -404,6 +476,8 @@ static void release(dgdiff_s *H) {
   cudaFree(H->d_src);
   cudaFree(H->d_mom);
   cudaFree(H->d_out);
+  cudaFree(H->d_mix);
+  cudaFree(H->d_mix_out);
   if (H->comm && g_nccl.commDestroy) g_nccl.commDestroy(H->comm);
   if (H->own_stream && H->stream) cudaStreamDestroy(H->stream);
   delete H;
@@ -575,6 +649,16 @@ static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
     for (int q = 0; q < 6; q++)
       for (int j = 0; j < H->d; j++) W[(t * 6 + q) * DMAXK + j] = H->tab.W[(t * 6 + q) * H->d + j];
   CK(cudaMemcpyToSymbol(c_W, W, sizeof W));
+  double CWv[2 * DMAXK] = {0};
+  for (int t = 0; t < 2; t++)
+    for (int j = 0; j < H->d; j++) CWv[t * DMAXK + j] = H->tab.cw[t * H->d + j];
+  CK(cudaMemcpyToSymbol(c_CW, CWv, sizeof CWv));
+  if (H->o.mixture_radius > 0) {
+    H->mix_R = H->o.mixture_radius;
+    const size_t nc = (size_t)(2 * H->mix_R + 1) * (2 * H->mix_R + 1);
+    CK(cudaMalloc(&H->d_mix, nc * sizeof(double)));
+    CK(cudaMalloc(&H->d_mix_out, (nc + 1) * sizeof(double)));
+  }
   CK(cudaMalloc(&H->d_out, 8 * sizeof(double)));
   // NCCL
   if (H->o.nranks > 1) {
@@ -611,6 +695,7 @@ extern "C" dgdiff_status dgdiff_create(dgdiff_t *out, const uint8_t *mask, int32
   if (o.nranks < 1 || o.rank < 0 || o.rank >= o.nranks) return fail(DGDIFF_E_ARG, "bad rank/nranks");
   if (o.temporal_steps < 0) return fail(DGDIFF_E_ARG, "temporal_steps < 0");
   if (o.max_chunk < 0) return fail(DGDIFF_E_ARG, "max_chunk < 0");
+  if (o.mixture_radius < 0 || o.mixture_radius > 2048) return fail(DGDIFF_E_ARG, "mixture_radius must be in [0, 2048]");
   dgdiff_s *H = new dgdiff_s();
   H->nx = nx; H->ny = ny; H->h = h; H->D = D; H->p = degree;
   H->d = (degree + 1) * (degree + 2) / 2;
@@ -775,6 +860,12 @@ after_stepping:
                                                chunk);
   k_mom_reduce<<<(int)((nvalid + 127) / 128), 128, 0, st>>>(H->d_partial, nblk, chunk, nvalid, H->h, mom_rows);
   H->st.launches += 2;
+  if (H->mix_R > 0) {
+    const int nc = (2 * H->mix_R + 1) * (2 * H->mix_R + 1);
+    k_mixture<T, NV, D2><<<(nc + 127) / 128, 128, 0, st>>>(u, H->d_aidx, H->nx, H->ny, nact, H->d_src_ij, mom_rows,
+                                                         nvalid, H->mix_R, H->d_mix);
+    H->st.launches++;
+  }
   CK(cudaGetLastError());
   return DGDIFF_OK;
 }
@@ -830,6 +921,12 @@ extern "C" dgdiff_status dgdiff_solve_batch(dgdiff_t H, const int32_t *sources, 
     H->mom_cap = n;
   }
   CK(cudaMemsetAsync(H->d_mom, 0, sizeof(double) * 6 * n, H->stream));
+  if (H->mix_R > 0) {
+    const size_t nc = (size_t)(2 * H->mix_R + 1) * (2 * H->mix_R + 1);
+    CK(cudaMemsetAsync(H->d_mix, 0, nc * sizeof(double), H->stream));
+  }
+  H->mix_reduced = false;
+  H->have_sigma = false;
   if (n > H->src_cap) {
     cudaFree(H->d_src);
     H->d_src = nullptr;
@@ -921,9 +1018,52 @@ extern "C" dgdiff_status dgdiff_covariance(dgdiff_t H, double delta, double sigm
   sigma[1] = out[1];
   sigma[2] = out[1];
   sigma[3] = out[2];
+  H->last_sigma[0] = out[0];
+  H->last_sigma[1] = out[1];
+  H->last_sigma[2] = out[2];
+  H->last_mu[0] = out[3];
+  H->last_mu[1] = out[4];
+  H->have_sigma = true;
   if (mu) {
     mu[0] = out[3];
     mu[1] = out[4];
+  }
+  return DGDIFF_OK;
+}
+
+extern "C" dgdiff_status dgdiff_mixture(dgdiff_t H, double *grid, double *residual) {
+  if (!H) return fail(DGDIFF_E_ARG, "handle is NULL");
+  if (H->mix_R <= 0) return fail(DGDIFF_E_STATE, "create the handle with opts.mixture_radius > 0");
+  if (!H->solved || !H->have_sigma) return fail(DGDIFF_E_STATE, "dgdiff_mixture needs dgdiff_covariance first");
+  CK(cudaSetDevice(H->dev));
+  const int R = H->mix_R;
+  const size_t nc = (size_t)(2 * R + 1) * (2 * R + 1);
+  if (H->o.nranks > 1 && !H->mix_reduced) {
+    ncclResult_t r = g_nccl.allReduce(H->d_mix, H->d_mix, nc, ncclFloat64, ncclSum, H->comm, H->stream);
+    if (r != ncclSuccess) return fail(DGDIFF_E_NCCL, "ncclAllReduce (mixture): %s", g_nccl.errStr(r));
+    H->mix_reduced = true;
+  }
+  k_mixture_final<<<1, 256, 0, H->stream>>>(H->d_mix, R, H->h, H->last_n, H->last_sigma[0], H->last_sigma[1],
+                                            H->last_sigma[2], H->last_mu[0], H->last_mu[1], H->d_mix_out,
+                                            H->d_mix_out + nc);
+  H->st.launches++;
+  CK(cudaGetLastError());
+  if (grid) CK(cudaMemcpyAsync(grid, H->d_mix_out, nc * sizeof(double), cudaMemcpyDeviceToHost, H->stream));
+  double res = 0;
+  CK(cudaMemcpyAsync(&res, H->d_mix_out + nc, sizeof(double), cudaMemcpyDeviceToHost, H->stream));
+  CK(cudaStreamSynchronize(H->stream));
+  if (residual) *residual = res;
+  return DGDIFF_OK;
+}
+
+extern "C" dgdiff_status dgdiff_centre_weights(int32_t degree, double *cw) {
+  if (degree < 1 || degree > 2) return fail(DGDIFF_E_ARG, "degree %d not supported (1 or 2)", degree);
+  if (!cw) return fail(DGDIFF_E_ARG, "cw is NULL");
+  try {
+    dgop::Table T = dgop::build(degree);
+    memcpy(cw, T.cw.data(), T.cw.size() * sizeof(double));
+  } catch (std::exception &e) {
+    return fail(DGDIFF_E_ARG, "operator precompute failed: %s", e.what());
   }
   return DGDIFF_OK;
 }

@@ -363,6 +363,10 @@ Table build(int p) {
       for (int j = 0; j < d; j++) s += R.Minv[t][i][j] * peval(R.phi[t][j], Q(1, 2), Q(1, 2));
       T.init[t * d + i] = (s * Q(1, 2)).to_double();
     }
+  // node value at the pixel centre (the diagonal's midpoint, shared by L and U)
+  T.cw.assign((size_t)2 * d, 0.0);
+  for (int t = 0; t < 2; t++)
+    for (int j = 0; j < d; j++) T.cw[t * d + j] = peval(R.phi[t][j], Q(1, 2), Q(1, 2)).to_double();
   return T;
 }
 

@@ -10,6 +10,7 @@ struct Table {
   std::vector<double> W;    // [2][6][d] moment weights on the unit pixel
   std::vector<double> init; // [2][d] projected Dirac at the pixel centre, units 1/h^2
   std::vector<int> nnz;     // [16][5] structural non-zeros per block
+  std::vector<double> cw;   // [2][d] N_j at the pixel centre (1/2, 1/2) (mixture node values)
 };
 
 // Throws std::runtime_error on failure (unsupported degree, non-dyadic entry,

@@ -21,14 +21,15 @@ STATUS_NAMES = ["OK", "E_ARG", "E_SOURCE", "E_UNSTABLE", "E_NONFINITE", "E_STATE
 EXPORTED = ["dgdiff_opts_default", "dgdiff_create", "dgdiff_solve_batch", "dgdiff_covariance",
             "dgdiff_source_moments", "dgdiff_get_density", "dgdiff_dt_max", "dgdiff_last_error",
             "dgdiff_destroy", "dgdiff_operator_table", "dgdiff_shard", "dgdiff_set_timing",
-            "dgdiff_get_stats", "dgdiff_reset_stats"]
+            "dgdiff_get_stats", "dgdiff_reset_stats", "dgdiff_mixture", "dgdiff_centre_weights"]
 
 
 class dgdiff_opts(ctypes.Structure):
     _fields_ = [("precision", ctypes.c_int32), ("outer_bc", ctypes.c_int32), ("centering", ctypes.c_int32),
                 ("temporal_steps", ctypes.c_int32), ("device", ctypes.c_int32), ("rank", ctypes.c_int32),
                 ("nranks", ctypes.c_int32), ("nccl_id", ctypes.c_void_p), ("keep_density", ctypes.c_int32),
-                ("max_chunk", ctypes.c_int32), ("stream", ctypes.c_void_p), ("kernel", ctypes.c_int32)]
+                ("max_chunk", ctypes.c_int32), ("stream", ctypes.c_void_p), ("kernel", ctypes.c_int32),
+                ("mixture_radius", ctypes.c_int32)]
 
 
 class dgdiff_stats_t(ctypes.Structure):
@@ -71,9 +72,11 @@ def _load():
     L.dgdiff_set_timing.argtypes = [H, i32]
     L.dgdiff_get_stats.argtypes = [H, ctypes.POINTER(dgdiff_stats_t)]
     L.dgdiff_reset_stats.argtypes = [H]
+    L.dgdiff_mixture.argtypes = [H, dp, dp]
+    L.dgdiff_centre_weights.argtypes = [i32, dp]
     for f in ("dgdiff_create", "dgdiff_solve_batch", "dgdiff_covariance", "dgdiff_source_moments",
               "dgdiff_get_density", "dgdiff_operator_table", "dgdiff_set_timing", "dgdiff_get_stats",
-              "dgdiff_reset_stats"):
+              "dgdiff_reset_stats", "dgdiff_mixture", "dgdiff_centre_weights"):
         getattr(L, f).restype = ctypes.c_int
     return L
 
@@ -160,6 +163,19 @@ def dgdiff_shard(n, rank, nranks):
     return b.value, e.value
 
 
+def dgdiff_mixture(handle, R):
+    grid = np.zeros((2 * R + 1, 2 * R + 1))
+    res = np.zeros(1)
+    _check(lib.dgdiff_mixture(handle, _dp(grid), _dp(res)))
+    return grid, float(res[0])
+
+
+def dgdiff_centre_weights(degree):
+    cw = np.zeros((2, ndof(degree)))
+    _check(lib.dgdiff_centre_weights(int(degree), _dp(cw)))
+    return cw
+
+
 def dgdiff_set_timing(handle, enable):
     _check(lib.dgdiff_set_timing(handle, int(bool(enable))))
 
@@ -203,6 +219,10 @@ class Solver:
 
     def moments(self):
         return dgdiff_source_moments(self.handle, self.n)
+
+    def mixture(self):
+        """(grid [(2R+1)][(2R+1)], Eq. (9) residual); needs mixture_radius=R."""
+        return dgdiff_mixture(self.handle, self.opts.mixture_radius)
 
     def density(self, src):
         return dgdiff_get_density(self.handle, src, self.nx, self.ny, self.degree)

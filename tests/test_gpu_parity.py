@@ -289,3 +289,29 @@ def test_c5_p2_sampled_parity(dg, orc, cfg):
     assert mom_err(mom[pick], ref_m) <= 1e-10
     assert np.abs(mom[:, 0] - 1).max() <= 1e-12
     assert S[0, 1] == S[1, 0]
+
+
+@pytest.mark.parametrize("prec,p", [(64, 1), (32, 1), (64, 2)])
+def test_mixture_grid_and_residual(dg, orc, prec, p):
+    """N2: the mixture grid and Eq. (9) residual vs the
+    oracle on a random mask with walls, several chunks, ragged batch."""
+    rng = np.random.default_rng(500 + prec + p)
+    mk = (rng.random((48, 44)) < 0.35).astype(np.uint8)
+    free = np.argwhere(mk[12:36, 12:32] == 0) + 12
+    G = 64 if p == 1 and prec == 64 else (128 if p == 1 else 32)
+    n = G + 5
+    pick = free[rng.integers(0, len(free), n)]
+    src = np.stack([pick[:, 1], pick[:, 0]], 1).astype(np.int32)
+    dt = 1 / 32 if p == 1 else 1 / 128
+    R = 12
+    ref_m, ref_d = orc.solve(p, 1.0, 1.0, mk, src, dt, 50, keep_density=True)
+    ref_g = orc.mixture(p, ref_d, src, ref_m, R)
+    S_ref, mu_ref = orc.sigma(ref_m)
+    ref_res = orc.residual(ref_g, 1.0, S_ref, mu_ref)
+    with dg.Solver(mk, 1.0, 1.0, p, precision=prec, mixture_radius=R, max_chunk=G) as s:
+        s.solve(src, dt, 50)
+        S, mu = s.covariance()
+        g, res = s.mixture()
+    tol = 1e-12 if prec == 64 else 1e-5
+    assert rel_l2(g, ref_g) <= tol
+    assert abs(res - ref_res) <= (1e-10 if prec == 64 else 1e-3) * ref_res

@@ -359,3 +359,59 @@ def test_convergence_order_smooth_gaussian(orc, p, ns, dtf, lo_, hi_):
         errs.append(orc.l2_err_gaussian(p, h, u, L / 2, L / 2, s2 + 2 * D * T))
     orders = [np.log2(errs[k] / errs[k + 1]) for k in range(len(errs) - 1)]
     assert all(lo_ <= o <= hi_ for o in orders), (errs, orders)
+
+
+# ---------------------------------------------------------------- mixture + Eq. (9) residual (N2)
+def test_mixture_dirac_node_value(orc):
+    """At t = 0 the P1 projected Dirac is +-3/h^2 on the source pixel; its
+    centre value (mean of the L and U traces at the diagonal midpoint) is
+    (3 + 3)/2 = 3/h^2 (R20), and every other node is 0."""
+    h = 0.5
+    mom, dens = orc.solve(1, h, 1.0, np.zeros((9, 9), np.uint8), [(4, 4)], 0.01, 0, keep_density=True)
+    g = orc.mixture(1, dens, [(4, 4)], mom, 3)
+    assert abs(g[3, 3] - 3 / h ** 2) <= 1e-14 * 12
+    g[3, 3] = 0
+    assert np.abs(g).max() == 0.0
+
+
+def test_mixture_free_space_is_gaussian(orc):
+    """Free space, P2 (Sigma = 2 D Delta I exactly): the mixture nodes integrate
+    to 1 and carry the second moment 2 D Delta by the midpoint rule (O(h^2/sigma^2)),
+    and the Eq. (9) residual is small against sum N^2.  (P2 tails reach ~23
+    sigma, so sources at different wall distances agree only to
+    ~1e-6 here; exact translation invariance is pinned with P1 below.)"""
+    n = 72
+    mask = np.zeros((n, n), np.uint8)
+    src = [(36, 36), (34, 37), (38, 35)]
+    mom, dens = orc.solve(2, 1.0, 1.0, mask, src, 1 / 128, 1024, keep_density=True)   # Delta = 8, sigma = 4
+    R = 24
+    g = orc.mixture(2, dens, src, mom, R)
+    g1 = orc.mixture(2, dens[:1], src[:1], mom[:1], R)
+    assert np.abs(g - g1).max() <= 1e-5 * g1.max()
+    assert abs(g.sum() - 1.0) < 2e-3
+    x = np.arange(-R, R + 1)
+    assert abs((g.sum(axis=0) * x ** 2).sum() - 16.0) < 0.1     # midpoint rule, truncated at 6 sigma
+    S, mu = orc.sigma(mom)
+    res = orc.residual(g, 1.0, S, mu)
+    X, Y = np.meshgrid(x, x)
+    gauss = np.exp(-(X ** 2 + Y ** 2) / 32.0) / (2 * np.pi * 16.0)
+    assert res < 1e-3 * (gauss ** 2).sum()
+    # Eq. (9) itself: the fitted Gaussian sampled at the nodes has zero residual
+    Si = np.linalg.inv(S)
+    dX, dY = X - mu[0], Y - mu[1]
+    fit = np.exp(-0.5 * (Si[0, 0] * dX ** 2 + 2 * Si[0, 1] * dX * dY + Si[1, 1] * dY ** 2)) / (
+        2 * np.pi * np.sqrt(np.linalg.det(S)))
+    assert orc.residual(fit, 1.0, S, mu) < 1e-28
+
+
+def test_mixture_translation_invariance_p1(orc):
+    """P1, Delta = 2 (sigma = 2), walls > 15 sigma away: the mixture of shifted
+    sources equals the single-source grid to rounding (catches a source/offset
+    index mix-up in the centring)."""
+    n = 80
+    mask = np.zeros((n, n), np.uint8)
+    src = [(40, 40), (37, 43), (44, 38)]
+    mom, dens = orc.solve(1, 1.0, 1.0, mask, src, 1 / 32, 64, keep_density=True)
+    g = orc.mixture(1, dens, src, mom, 10)
+    g1 = orc.mixture(1, dens[:1], src[:1], mom[:1], 10)
+    assert np.abs(g - g1).max() <= 1e-12 * g1.max()
