@@ -336,6 +336,8 @@ struct dgdiff_s {
   int4 *d_nbr = nullptr;
   int4 *d_rowtab = nullptr;  // [nstrips][ny] {h0, c0, c1, h1} for the ring kernel
   int4 *d_rowtab3 = nullptr; // [nstrips3][ny][2] u/U1/U2/output bounds for the fused step
+  int4 *d_rowtab_na = nullptr; // ring row table of the stage without the alpha term
+  int nstrips_na = 0;
   int nstrips3 = 0;
   double macs_per_stage = 0; // structural MACs of one stage over all active pixels (per source)
   int nstrips = 0, ring_w = 0, nsm = 148;
@@ -467,6 +469,7 @@ static void release(dgdiff_s *H) {
   cudaFree(H->d_nbr);
   cudaFree(H->d_rowtab);
   cudaFree(H->d_rowtab3);
+  cudaFree(H->d_rowtab_na);
   cudaFree(H->d_pix);
   cudaFree(H->d_aidx);
   cudaFree(H->d_A);
@@ -558,11 +561,9 @@ static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
     int i = pix[a].x, j = pix[a].y;
     nbr[a] = make_int4(at(i + 1, j), at(i - 1, j), at(i, j + 1), at(i, j - 1));
   }
-  // ring kernel row table: active-index bounds of every (strip, row) tile
+  // ring kernel row tables (one per strip width: the stage without the alpha
+  // term may use wider strips): active-index bounds of every (strip, row) tile
   if (use_ring(H)) {
-    H->ring_w = dgl::ring_width(H->p);
-    const int W = H->ring_w;
-    H->nstrips = (nx + W - 1) / W;
     std::vector<int> cum((size_t)ny * (nx + 1));
     int run = 0;
     for (int j = 0; j < ny; j++) {
@@ -572,21 +573,35 @@ static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
       }
       cum[(size_t)j * (nx + 1) + nx] = run;
     }
-    std::vector<int4> rtab((size_t)H->nstrips * ny);
-    for (int s = 0; s < H->nstrips; s++)
-      for (int j = 0; j < ny; j++) {
-        const int x0 = s * W;
-        auto c = [&](int x) { return cum[(size_t)j * (nx + 1) + std::max(0, std::min(nx, x))]; };
-        rtab[(size_t)s * ny + j] = make_int4(c(x0 - 1), c(x0), c(x0 + W), c(x0 + W + 1));
+    for (int va = 0; va < 2; va++) {
+      const bool alpha = va == 1;
+      const int W = dgl::ring_width(H->p, alpha);
+      const int ns = (nx + W - 1) / W;
+      std::vector<int4> rtab((size_t)ns * ny);
+      for (int s = 0; s < ns; s++)
+        for (int j = 0; j < ny; j++) {
+          const int x0 = s * W;
+          auto c = [&](int x) { return cum[(size_t)j * (nx + 1) + std::max(0, std::min(nx, x))]; };
+          rtab[(size_t)s * ny + j] = make_int4(c(x0 - 1), c(x0), c(x0 + W), c(x0 + W + 1));
+        }
+      // mean halo.d row-tile size (pixel tiles): the ring kernel without the
+      // alpha term keeps ~8 mean rows in flight (measured optimum on c2/c4:
+      // deeper TMA queues delay the row the consumers need next)
+      double tiles = 0;
+      for (const int4 &t : rtab) tiles += t.w - t.x;
+      int4 *d = nullptr;
+      CK(cudaMalloc(&d, sizeof(int4) * rtab.size()));
+      CK(cudaMemcpy(d, rtab.data(), sizeof(int4) * rtab.size(), cudaMemcpyHostToDevice));
+      if (alpha) {
+        H->d_rowtab = d;
+        H->nstrips = ns;
+        H->ring_w = W;
+      } else {
+        H->d_rowtab_na = d;
+        H->nstrips_na = ns;
+        H->mean_tile = tiles / (double)std::max<size_t>(1, rtab.size());
       }
-    // mean halo'd row-tile size (pixel tiles): the ring kernel without the
-    // alpha term keeps ~8 mean rows in flight (measured optimum on c2/c4:
-    // deeper TMA queues delay the row the consumers need next)
-    double tiles = 0;
-    for (const int4 &t : rtab) tiles += t.w - t.x;
-    H->mean_tile = tiles / (double)std::max<size_t>(1, rtab.size());
-    CK(cudaMalloc(&H->d_rowtab, sizeof(int4) * rtab.size()));
-    CK(cudaMemcpy(H->d_rowtab, rtab.data(), sizeof(int4) * rtab.size(), cudaMemcpyHostToDevice));
+    }
   }
   // fused-step row table (P1): bounds of the u (3-column halo), U1 (2), U2 (1)
   // and output ranges of every (strip, row)
@@ -781,7 +796,10 @@ static dgdiff_status run_chunk(dgdiff_s *H, int64_t nvalid, int64_t chunk, doubl
   sa.diag = H->o.kernel == 9 ? 1 : 0;
   sa.ahead_alpha = H->ahead_alpha;
   sa.ahead_noalpha = H->ahead_noalpha;
-  sa.n1_use = H->n1_use > 0 ? H->n1_use : (int)(8.0 * H->mean_tile + 0.5);
+  sa.n1_use = H->n1_use;
+  sa.n1_use_na = H->n1_use > 0 ? H->n1_use : (int)(8.0 * H->mean_tile + 0.5);
+  sa.rowtab_na = H->d_rowtab_na;
+  sa.nstrips_na = H->nstrips_na;
   sa.n2_use = H->n2_use;
   sa.st = st;
   const int which = H->o.kernel == 1 ? 0 : H->o.kernel == 2 ? 1 : 2;

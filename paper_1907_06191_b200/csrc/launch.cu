@@ -5,7 +5,10 @@
 
 namespace dgl {
 
-int ring_width(int P) { return P == 1 ? dgk::RingCfg<1, 16>::W : dgk::RingCfg<2, 8>::W; }
+int ring_width(int P, bool alpha) {
+  if (P == 1) return alpha ? dgk::RingCfg<1, 16, true>::W : dgk::RingCfg<1, 16, false>::W;
+  return alpha ? dgk::RingCfg<2, 8, true>::W : dgk::RingCfg<2, 8, false>::W;
+}
 
 cudaError_t launch_stage(int which, int prec, int P, bool alpha, const StageArgs &a) {
   if (which == 0 || which == 1)

@@ -12,6 +12,8 @@ struct StageArgs {
   const int4 *nbr = nullptr;
   const void *A = nullptr;          // v1 only: operator table in global memory
   const int4 *rowtab = nullptr;     // ring only: [nstrips][ny] {h0, c0, c1, h1}
+  const int4 *rowtab_na = nullptr;  // ring, no-alpha stage: its own strip width
+  int nstrips_na = 0, n1_use_na = 0;
   int nact = 0, ny = 0, nstrips = 0, ngroups = 0, nsm = 148;
   int px = 32, wpb = 4;             // v1/v2 mapping
   int diag = 0;                     // ring diagnostic (stream without compute)
@@ -24,7 +26,7 @@ struct StageArgs {
 // which: 0 = v1 (table in gmem), 1 = v2 (immediates), 2 = v3 ring (bulk TMA)
 cudaError_t launch_stage(int which, int prec, int P, bool alpha, const StageArgs &a);
 // strip width of the ring kernel for degree P (its row table depends on it)
-int ring_width(int P);
+int ring_width(int P, bool alpha);
 // K3: one fused SSP-RK3 step per pass (P1); a.rowtab = rowtab3 [nstrips][ny][2]
 cudaError_t launch_step_fused(int prec, const StageArgs &a);
 int fused_width(int prec);

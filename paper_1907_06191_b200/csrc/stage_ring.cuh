@@ -44,19 +44,22 @@ constexpr int RING_Q = 16;         // row entries (full/empty barrier pairs)
 #endif
 constexpr int RING_MAXBAND = 256;  // max rows per band (+2 halo rows)
 
-// strip width W and consumer warps NC per (degree, lane bytes): a pixel tile is
-// 2d x 32 lanes x lane bytes; four full halo'd rows must fit in ring 1
-template <int P, int LB> struct RingCfg;
-template <> struct RingCfg<1, 8> { static constexpr int W = 16, NC = 16; };
-template <> struct RingCfg<1, 16> { static constexpr int W = 8, NC = 8; };  // NC swept: 4, 8, 12, 16 -> 8 best
-template <> struct RingCfg<2, 8> { static constexpr int W = 8, NC = 16; };
+// strip width W and consumer warps NC per (degree, lane bytes, alpha term): a
+// pixel tile is 2d x 32 lanes x lane bytes; four full halo'd rows must fit in
+// ring 1.  Without the alpha term ring 2 only holds neighbour indices, so the
+// P1 stage-1 kernel affords W = 16 (half the rows per byte of W = 8).
+template <int P, int LB, bool ALPHA> struct RingCfg;
+template <> struct RingCfg<1, 16, true> { static constexpr int W = 8, NC = 8; };   // NC swept 4/8/12/16
+template <> struct RingCfg<1, 16, false> { static constexpr int W = 16, NC = 8; };
+template <> struct RingCfg<2, 8, true> { static constexpr int W = 8, NC = 16; };
+template <> struct RingCfg<2, 8, false> { static constexpr int W = 8, NC = 16; };
 
 template <typename T, int NV, int P, bool ALPHA>
 struct RingGeom {
   static constexpr int G = 32 * NV;
   static constexpr int D2 = (P + 1) * (P + 2);
-  static constexpr int W = RingCfg<P, NV * (int)sizeof(T)>::W;
-  static constexpr int NC = RingCfg<P, NV * (int)sizeof(T)>::NC;
+  static constexpr int W = RingCfg<P, NV * (int)sizeof(T), ALPHA>::W;
+  static constexpr int NC = RingCfg<P, NV * (int)sizeof(T), ALPHA>::NC;
   static constexpr int PXB = D2 * G * (int)sizeof(T);  // one pixel tile (one group)
   static constexpr int SMEM_MAX = 232448;
   static constexpr int EXTRA = 2 * RING_Q * 8 + RING_Q * 32 + (RING_MAXBAND + 2) * 16 + 2 * RING_Q * 4;
@@ -334,7 +337,7 @@ cudaError_t launch_ring(const dgl::StageArgs &a) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int per_band = a.nstrips * a.ngroups;
+  const int per_band = (ALPHA ? a.nstrips : a.nstrips_na) * a.ngroups;
   int nbands = std::max(1, std::min(a.ny, (8 * a.nsm + per_band - 1) / per_band));
   int band_rows = (a.ny + nbands - 1) / nbands;
   if (band_rows > RING_MAXBAND) band_rows = RING_MAXBAND;
@@ -342,10 +345,11 @@ cudaError_t launch_ring(const dgl::StageArgs &a) {
   const int nitems = per_band * nbands;
   const int grid = std::min(nitems, a.nsm);
   k_stage_ring<T, NV, P, ALPHA><<<grid, Gm::THREADS, Gm::SMEM + pad, a.st>>>(
-      (const T *)a.Uin, (const T *)a.U0, (T *)a.Uout, a.nbr, a.rowtab, a.nact, a.ny, a.nstrips, a.ngroups,
+      (const T *)a.Uin, (const T *)a.U0, (T *)a.Uout, a.nbr, ALPHA ? a.rowtab : a.rowtab_na, a.nact, a.ny,
+      ALPHA ? a.nstrips : a.nstrips_na, a.ngroups,
       band_rows, nitems, (T)a.alpha, (T)a.cs, a.diag,
       std::max(4, std::min(RING_Q - 1, alpha_max_ahead(a, ALPHA))),
-      ALPHA ? Gm::N1 : std::max(4 * (Gm::W + 2), std::min(Gm::N1, a.n1_use > 0 ? a.n1_use : Gm::N1)),
+      ALPHA ? Gm::N1 : std::max(4 * (Gm::W + 2), std::min(Gm::N1, a.n1_use_na > 0 ? a.n1_use_na : Gm::N1)),
       std::max(4 * Gm::W, std::min(Gm::N2, a.n2_use > 0 ? a.n2_use : Gm::N2)));
   return cudaGetLastError();
 }
