@@ -62,7 +62,8 @@ typedef struct {
   int32_t device;         /* CUDA device ordinal; -1 = current device */
   int32_t rank, nranks;   /* source sharding: rank takes the contiguous block
                              [rank*n/nranks, (rank+1)*n/nranks) of every batch */
-  const void *nccl_id;    /* ncclUniqueId* (128 bytes), required iff nranks > 1 */
+  const void *nccl_id;    /* ncclUniqueId* (128 bytes), required if nranks > 1;
+                             with nranks == 1 it creates a one-rank communicator */
   int32_t keep_density;   /* 1: keep the final states of the last source chunk for
                              dgdiff_get_density (tests); 0 (default) */
   int32_t max_chunk;      /* max sources resident per chunk; 0 = fit device memory */

@@ -676,7 +676,9 @@ static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
   }
   CK(cudaMalloc(&H->d_out, 8 * sizeof(double)));
   // NCCL
-  if (H->o.nranks > 1) {
+  // NCCL communicator: required when nranks > 1; with nranks == 1 an explicit
+  // nccl_id also creates one (a one-rank world: exercises the same path)
+  if (H->o.nranks > 1 || H->o.nccl_id) {
     if (!H->o.nccl_id) return fail(DGDIFF_E_ARG, "nranks > 1 needs opts.nccl_id");
     if (!g_nccl.load()) return fail(DGDIFF_E_NCCL, "cannot load libnccl.so.2: %s", dlerror());
     ncclUniqueId id;
@@ -1017,7 +1019,7 @@ extern "C" dgdiff_status dgdiff_covariance(dgdiff_t H, double delta, double sigm
     return fail(DGDIFF_E_STATE, "delta = %.17g but the last solve reached nsteps*dt = %.17g", delta, t);
   CK(cudaSetDevice(H->dev));
   const int64_t n = H->last_n;
-  if (H->o.nranks > 1) {
+  if (H->comm) {
     // the one cross-GPU step: sum of disjoint zero-padded rows is exact
     ncclResult_t r = g_nccl.allReduce(H->d_mom, H->d_mom, (size_t)6 * n, ncclFloat64, ncclSum, H->comm, H->stream);
     if (r != ncclSuccess) return fail(DGDIFF_E_NCCL, "ncclAllReduce: %s", g_nccl.errStr(r));
@@ -1056,7 +1058,7 @@ extern "C" dgdiff_status dgdiff_mixture(dgdiff_t H, double *grid, double *residu
   CK(cudaSetDevice(H->dev));
   const int R = H->mix_R;
   const size_t nc = (size_t)(2 * R + 1) * (2 * R + 1);
-  if (H->o.nranks > 1 && !H->mix_reduced) {
+  if (H->comm && !H->mix_reduced) {
     ncclResult_t r = g_nccl.allReduce(H->d_mix, H->d_mix, nc, ncclFloat64, ncclSum, H->comm, H->stream);
     if (r != ncclSuccess) return fail(DGDIFF_E_NCCL, "ncclAllReduce (mixture): %s", g_nccl.errStr(r));
     H->mix_reduced = true;

@@ -315,3 +315,24 @@ def test_mixture_grid_and_residual(dg, orc, prec, p):
     tol = 1e-12 if prec == 64 else 1e-5
     assert rel_l2(g, ref_g) <= tol
     assert abs(res - ref_res) <= (1e-10 if prec == 64 else 1e-3) * ref_res
+
+
+def test_nccl_one_rank_world(dg, cfg):
+    """The multi-GPU code path on one device: a one-rank NCCL communicator
+    (dlopen, ncclCommInitRank, the moment-table and mixture all-reduces) gives
+    bitwise the same Sigma and mixture as the communicator-free path."""
+    import torch
+    m = cfg.mask("c1")
+    rng = np.random.default_rng(11)
+    free = np.argwhere(m == 0)
+    pick = free[rng.integers(0, len(free), 70)]
+    src = np.stack([pick[:, 1], pick[:, 0]], 1).astype(np.int32)
+    out = []
+    for nid in (None, torch.cuda.nccl.unique_id()):
+        with dg.Solver(m, 1.0, 1.0, 1, nccl_id=nid, mixture_radius=6) as s:
+            s.solve(src, 1 / 32, 30)
+            S, mu = s.covariance()
+            g, res = s.mixture()
+            out.append((S, mu, g, res))
+    for a, b in zip(out[0], out[1]):
+        assert np.array_equal(a, b)
