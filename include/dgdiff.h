@@ -52,7 +52,10 @@ typedef struct {
                              of the stencil sum; moments always accumulate in fp64 */
   int32_t outer_bc;       /* 0 = REFLECT (default): the outer square acts as an
                              axon wall (reading R9).  1 = ABSORB, Eq. (4)
-                             (P:67-70): not implemented on the GPU path -> E_ARG */
+                             (P:67-70): u = 0 on the outer square (ghost u+ = -u-);
+                             mass leaves the grid.  ABSORB runs on the default
+                             ring kernel only (kernel 1/2 or temporal_steps 2 ->
+                             E_ARG) */
   int32_t centering;      /* 0 = shift each density by its source point (default,
                              reading R12); 1 = by its own mean */
   int32_t temporal_steps; /* 0 = library choice; 1 = one launch per RK stage
@@ -163,6 +166,12 @@ void dgdiff_destroy(dgdiff_t);
  *  init [2][d]:  the projected Dirac at the pixel centre times h^2.
  * Any pointer may be NULL. */
 dgdiff_status dgdiff_operator_table(int32_t degree, double *A, double *W, double *init);
+
+/* Composite blocks of pixels with absorbing outer faces (outer_bc = 1,
+ * Eq. (4)): A [16][16][5][2d][2d] indexed [code][outer] with outer the 4-bit
+ * set of the pixel's faces on the outer square (same bit order as code); only
+ * entries with code & outer == 0 and outer != 0 are used.  Units D/h^2. */
+dgdiff_status dgdiff_absorb_table(int32_t degree, double *A);
 
 /* Values at the pixel centre (1/2, 1/2) of the unit pixel's basis functions,
  * cw [2][d] (triangle-major, canonical order): the mixture node weights. */

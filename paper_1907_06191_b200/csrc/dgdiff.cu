@@ -345,6 +345,7 @@ struct dgdiff_s {
   int *d_aidx = nullptr;
   std::vector<int> h_aidx;
   void *d_A = nullptr;
+  void *d_Aabs = nullptr;  // ABSORB boundary-pixel blocks (state precision)
   dgop::Table tab;
   // chunk buffers
   void *d_U[3] = {nullptr, nullptr, nullptr};
@@ -473,6 +474,7 @@ static void release(dgdiff_s *H) {
   cudaFree(H->d_pix);
   cudaFree(H->d_aidx);
   cudaFree(H->d_A);
+  cudaFree(H->d_Aabs);
   cudaFree(H->d_src_a);
   cudaFree(H->d_src_ij);
   cudaFree(H->d_partial);
@@ -556,7 +558,12 @@ static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
   H->h_aidx = aidx;
   if (H->nact == 0) return fail(DGDIFF_E_ARG, "substrate has no extracellular pixel");
   std::vector<int4> nbr(H->nact);
-  auto at = [&](int i, int j) { return (i < 0 || j < 0 || i >= nx || j >= ny) ? -1 : aidx[(size_t)j * nx + i]; };
+  // neighbour index: active index, -1 for an axon pixel (or the outer square
+  // under REFLECT, reading R9), -2 for a face on the outer square under ABSORB
+  const int outside = H->o.outer_bc == 1 ? -2 : -1;
+  auto at = [&](int i, int j) {
+    return (i < 0 || j < 0 || i >= nx || j >= ny) ? outside : aidx[(size_t)j * nx + i];
+  };
   for (int64_t a = 0; a < H->nact; a++) {
     int i = pix[a].x, j = pix[a].y;
     nbr[a] = make_int4(at(i + 1, j), at(i - 1, j), at(i, j + 1), at(i, j - 1));
@@ -659,6 +666,22 @@ static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
     CK(cudaMalloc(&H->d_A, na * sizeof(double)));
     CK(cudaMemcpy(H->d_A, H->tab.A.data(), na * sizeof(double), cudaMemcpyHostToDevice));
   }
+  if (H->o.outer_bc == 1) {
+    std::vector<double> Ab;
+    try {
+      Ab = dgop::build_absorb(H->p);
+    } catch (std::exception &ex) {
+      return fail(DGDIFF_E_ARG, "absorbing operator precompute failed: %s", ex.what());
+    }
+    if (H->o.precision == 32) {
+      std::vector<float> A32(Ab.begin(), Ab.end());
+      CK(cudaMalloc(&H->d_Aabs, A32.size() * sizeof(float)));
+      CK(cudaMemcpy(H->d_Aabs, A32.data(), A32.size() * sizeof(float), cudaMemcpyHostToDevice));
+    } else {
+      CK(cudaMalloc(&H->d_Aabs, Ab.size() * sizeof(double)));
+      CK(cudaMemcpy(H->d_Aabs, Ab.data(), Ab.size() * sizeof(double), cudaMemcpyHostToDevice));
+    }
+  }
   double W[2 * 6 * DMAXK] = {0};
   for (int t = 0; t < 2; t++)
     for (int q = 0; q < 6; q++)
@@ -706,8 +729,9 @@ extern "C" dgdiff_status dgdiff_create(dgdiff_t *out, const uint8_t *mask, int32
   dgdiff_opts o;
   if (opts) o = *opts; else dgdiff_opts_default(&o);
   if (o.precision != 32 && o.precision != 64) return fail(DGDIFF_E_ARG, "precision must be 32 or 64");
-  if (o.outer_bc != 0)
-    return fail(DGDIFF_E_ARG, "outer_bc ABSORB (Eq. (4)) is not implemented on the GPU path; REFLECT only");
+  if (o.outer_bc != 0 && o.outer_bc != 1) return fail(DGDIFF_E_ARG, "outer_bc must be 0 (REFLECT) or 1 (ABSORB)");
+  if (o.outer_bc == 1 && (o.kernel == 1 || o.kernel == 2 || o.temporal_steps == 2))
+    return fail(DGDIFF_E_ARG, "outer_bc ABSORB runs on the default ring kernel only");
   if (o.centering != 0 && o.centering != 1) return fail(DGDIFF_E_ARG, "centering must be 0 or 1");
   if (o.nranks < 1 || o.rank < 0 || o.rank >= o.nranks) return fail(DGDIFF_E_ARG, "bad rank/nranks");
   if (o.temporal_steps < 0) return fail(DGDIFF_E_ARG, "temporal_steps < 0");
@@ -787,6 +811,7 @@ static dgdiff_status run_chunk(dgdiff_s *H, int64_t nvalid, int64_t chunk, doubl
   dgl::StageArgs sa;
   sa.nbr = H->d_nbr;
   sa.A = A;
+  sa.Aabs = H->d_Aabs;
   sa.rowtab = H->d_rowtab;
   sa.nact = nact;
   sa.ny = H->ny;
@@ -1073,6 +1098,18 @@ extern "C" dgdiff_status dgdiff_mixture(dgdiff_t H, double *grid, double *residu
   CK(cudaMemcpyAsync(&res, H->d_mix_out + nc, sizeof(double), cudaMemcpyDeviceToHost, H->stream));
   CK(cudaStreamSynchronize(H->stream));
   if (residual) *residual = res;
+  return DGDIFF_OK;
+}
+
+extern "C" dgdiff_status dgdiff_absorb_table(int32_t degree, double *A) {
+  if (degree < 1 || degree > 2) return fail(DGDIFF_E_ARG, "degree %d not supported (1 or 2)", degree);
+  if (!A) return fail(DGDIFF_E_ARG, "A is NULL");
+  try {
+    std::vector<double> T = dgop::build_absorb(degree);
+    memcpy(A, T.data(), T.size() * sizeof(double));
+  } catch (std::exception &e) {
+    return fail(DGDIFF_E_ARG, "operator precompute failed: %s", e.what());
+  }
   return DGDIFF_OK;
 }
 

@@ -11,6 +11,7 @@ struct StageArgs {
   void *Uout = nullptr;
   const int4 *nbr = nullptr;
   const void *A = nullptr;          // v1 only: operator table in global memory
+  const void *Aabs = nullptr;       // ring, ABSORB: [16][16][5][2d][2d] boundary-pixel blocks
   const int4 *rowtab = nullptr;     // ring only: [nstrips][ny] {h0, c0, c1, h1}
   const int4 *rowtab_na = nullptr;  // ring, no-alpha stage: its own strip width
   int nstrips_na = 0, n1_use_na = 0;

@@ -261,7 +261,10 @@ static int tri_index(int di, int dj, int t) { return ((dj + 1) * 3 + (di + 1)) *
 
 static bool dyadic(const Q &q) { return (q.d & (q.d - 1)) == 0; }
 
-static void build_table(const RefEl &R, int code, Mat &out /* 2d x 18d */) {
+// outer: faces of the centre pixel that lie on the outer square under the
+// absorbing condition Eq. (4) (ghost u+ = -u-, q+ = q-, k+ = k-):
+// they contribute h_u = 0 to its q and the full k_T q- . n to its rhs.
+static void build_table(const RefEl &R, int code, Mat &out /* 2d x 18d */, int outer = 0) {
   const int d = R.d, N = 18 * d;
   // q_c of a triangle of the patch as a d x N matrix (first row of Eq. (7),
   // central u-flux; any neighbour's u may be nonzero)
@@ -271,6 +274,7 @@ static void build_table(const RefEl &R, int code, Mat &out /* 2d x 18d */) {
     for (int i = 0; i < d; i++)
       for (int j = 0; j < d; j++) rhs[i][T * d + j] = -R.Dc[t][c][i][j];
     for (int f = 0; f < 3; f++) {
+      if (di == 0 && dj == 0 && FACEBIT[t][f] >= 0 && ((outer >> FACEBIT[t][f]) & 1)) continue;  // h_u = 0
       int ni = di + NDI[t][f], nj = dj + NDJ[t][f];
       if (ni < -1 || ni > 1 || nj < -1 || nj > 1) throw std::runtime_error("patch too small");
       int Tn = tri_index(ni, nj, 1 - t);
@@ -293,6 +297,13 @@ static void build_table(const RefEl &R, int code, Mat &out /* 2d x 18d */) {
     // faces: k_f 1/2 sum_c nu_c (E- q_c + E+ q_c^nb), k_f = 1 if open else 0
     for (int f = 0; f < 3; f++) {
       int bit = FACEBIT[t][f];
+      if (bit >= 0 && ((outer >> bit) & 1)) {   // absorbing outer face: k_T q- . n, full weight
+        for (int c = 0; c < 2; c++) {
+          Q w = Q(NU[t][f][c]);
+          if (!w.zero()) axpy(r, w, mul(R.Em[t][f], q0[c]));
+        }
+        continue;
+      }
       if (bit >= 0 && !((code >> bit) & 1)) continue;
       int ni = NDI[t][f], nj = NDJ[t][f];
       for (int c = 0; c < 2; c++) {
@@ -368,6 +379,39 @@ Table build(int p) {
   for (int t = 0; t < 2; t++)
     for (int j = 0; j < d; j++) T.cw[t * d + j] = peval(R.phi[t][j], Q(1, 2), Q(1, 2)).to_double();
   return T;
+}
+
+std::vector<double> build_absorb(int p) {
+  if (p < 1 || p > 2) throw std::runtime_error("absorbing table: degree must be 1 or 2");
+  RefEl R;
+  build_ref(R, p);
+  const int d = R.d, D2 = 2 * d;
+  const int OFF[5][2] = {{0, 0}, {1, 0}, {-1, 0}, {0, 1}, {0, -1}};
+  std::vector<double> A((size_t)16 * 16 * 5 * D2 * D2, 0.0);
+  for (int code = 0; code < 16; code++)
+    for (int outer = 1; outer < 16; outer++) {
+      if (code & outer) continue;                    // a face is open or outer, not both
+      Mat full;
+      build_table(R, code, full, outer);
+      for (int dj = -1; dj <= 1; dj++)
+        for (int di = -1; di <= 1; di++) {
+          int o = -1;
+          for (int k = 0; k < 5; k++)
+            if (OFF[k][0] == di && OFF[k][1] == dj) o = k;
+          bool used = (o == 0) || (o > 0 && ((code >> (o - 1)) & 1));
+          for (int r = 0; r < D2; r++)
+            for (int t = 0; t < 2; t++)
+              for (int j = 0; j < d; j++) {
+                const Q &q = full[r][tri_index(di, dj, t) * d + j];
+                if (o < 0 || !used) {
+                  if (o < 0 && !q.zero()) throw std::runtime_error("absorbing: corner coupling is not zero");
+                  continue;
+                }
+                A[((((size_t)code * 16 + outer) * 5 + o) * D2 + r) * D2 + t * d + j] = q.to_double();
+              }
+        }
+    }
+  return A;
 }
 
 }  // namespace dgop

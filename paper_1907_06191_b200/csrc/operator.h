@@ -17,4 +17,9 @@ struct Table {
 // non-zero corner coupling, rational overflow).
 Table build(int p);
 
+// Composite blocks of pixels with absorbing outer faces (outer_bc = ABSORB,
+// Eq. (4)): A[code][outer][5][2d][2d] (outer = faces on the outer square; zero
+// unless code & outer == 0 and outer != 0), units D/h^2.
+std::vector<double> build_absorb(int p);
+
 }  // namespace dgop

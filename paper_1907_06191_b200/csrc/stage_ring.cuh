@@ -88,7 +88,8 @@ template <typename T, int NV, int P, bool HAS_ALPHA>
 __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
     k_stage_ring(const T *__restrict__ Uin, const T *U0, T *Uout, const int4 *__restrict__ nbr,
                  const int4 *__restrict__ rowtab, int nact, int ny, int nstrips, int ngroups, int band_rows,
-                 int nitems, T alpha, T cs, int diag, int max_ahead, int n1_use, int n2_use) {
+                 int nitems, T alpha, T cs, int diag, int max_ahead, int n1_use, int n2_use,
+                 const T *__restrict__ Aabs) {
   using Gm = RingGeom<T, NV, P, HAS_ALPHA>;
   constexpr int G = Gm::G, D2 = Gm::D2, PXB = Gm::PXB, Q = RING_Q, NC = Gm::NC;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -264,34 +265,52 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
       for (int k = 0; k < D2; k++)
 #pragma unroll
         for (int e = 0; e < NV; e++) acc[k][e] = (T)0;
-      // self block of this pixel's open-face code (compile-time immediates),
-      // then the fixed neighbour blocks of the open faces
-      mv_self<T, NV, P>(open_code(nb), acc, xs);
-      if (nb.x >= 0) {
-        const T *pn = tile1(mc, nb.x);
+      // faces on the outer square under ABSORB (Eq. (4)) are marked -2
+      const int outer = (nb.x == -2) | ((nb.y == -2) << 1) | ((nb.z == -2) << 2) | ((nb.w == -2) << 3);
+      if (__builtin_expect(outer == 0, 1)) {
+        // self block of this pixel's open-face code (compile-time immediates),
+        // then the fixed neighbour blocks of the open faces
+        mv_self<T, NV, P>(open_code(nb), acc, xs);
+        if (nb.x >= 0) {
+          const T *pn = tile1(mc, nb.x);
 #pragma unroll
-        for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
-        mv_imm<T, NV, P, 5>(acc, xn);
-      }
-      if (nb.y >= 0) {
-        const T *pn = tile1(mc, nb.y);
+          for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
+          mv_imm<T, NV, P, 5>(acc, xn);
+        }
+        if (nb.y >= 0) {
+          const T *pn = tile1(mc, nb.y);
 #pragma unroll
-        for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
-        mv_imm<T, NV, P, 6>(acc, xn);
-      }
-      if (nb.z >= 0) {
-        const RowMeta mn = meta[seq(j + 1) % Q];
-        const T *pn = tile1(mn, nb.z);
+          for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
+          mv_imm<T, NV, P, 6>(acc, xn);
+        }
+        if (nb.z >= 0) {
+          const RowMeta mn = meta[seq(j + 1) % Q];
+          const T *pn = tile1(mn, nb.z);
 #pragma unroll
-        for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
-        mv_imm<T, NV, P, 7>(acc, xn);
-      }
-      if (nb.w >= 0) {
-        const RowMeta ms = meta[seq(j - 1) % Q];
-        const T *pn = tile1(ms, nb.w);
+          for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
+          mv_imm<T, NV, P, 7>(acc, xn);
+        }
+        if (nb.w >= 0) {
+          const RowMeta ms = meta[seq(j - 1) % Q];
+          const T *pn = tile1(ms, nb.w);
 #pragma unroll
-        for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
-        mv_imm<T, NV, P, 8>(acc, xn);
+          for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
+          mv_imm<T, NV, P, 8>(acc, xn);
+        }
+      } else {
+        // boundary pixel with absorbing outer faces: blocks of (code, outer)
+        // read from the K0 table in global memory (rare: grid-edge pixels)
+        const T *Ab = Aabs + (size_t)((open_code(nb) * 16 + outer) * 5) * D2 * D2;
+        mv_gen<T, NV, D2>(acc, Ab, xs);
+        const int nbv[4] = {nb.x, nb.y, nb.z, nb.w};
+#pragma unroll 1
+        for (int f = 0; f < 4; f++) {
+          if (nbv[f] < 0) continue;
+          const T *pn = f < 2 ? tile1(mc, nbv[f]) : tile1(meta[seq(f == 2 ? j + 1 : j - 1) % Q], nbv[f]);
+#pragma unroll
+          for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
+          mv_gen<T, NV, D2>(acc, Ab + (size_t)(f + 1) * D2 * D2, xn);
+        }
       }
       const T *pu = reinterpret_cast<const T *>(ring2 + (size_t)sl2 * PXB) + lane * NV;
       T *out = Uog + (size_t)a * D2 * G;
@@ -350,7 +369,7 @@ cudaError_t launch_ring(const dgl::StageArgs &a) {
       band_rows, nitems, (T)a.alpha, (T)a.cs, a.diag,
       std::max(4, std::min(RING_Q - 1, alpha_max_ahead(a, ALPHA))),
       ALPHA ? Gm::N1 : std::max(4 * (Gm::W + 2), std::min(Gm::N1, a.n1_use_na > 0 ? a.n1_use_na : Gm::N1)),
-      std::max(4 * Gm::W, std::min(Gm::N2, a.n2_use > 0 ? a.n2_use : Gm::N2)));
+      std::max(4 * Gm::W, std::min(Gm::N2, a.n2_use > 0 ? a.n2_use : Gm::N2)), (const T *)a.Aabs);
   return cudaGetLastError();
 }
 

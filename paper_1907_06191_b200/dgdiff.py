@@ -21,7 +21,8 @@ STATUS_NAMES = ["OK", "E_ARG", "E_SOURCE", "E_UNSTABLE", "E_NONFINITE", "E_STATE
 EXPORTED = ["dgdiff_opts_default", "dgdiff_create", "dgdiff_solve_batch", "dgdiff_covariance",
             "dgdiff_source_moments", "dgdiff_get_density", "dgdiff_dt_max", "dgdiff_last_error",
             "dgdiff_destroy", "dgdiff_operator_table", "dgdiff_shard", "dgdiff_set_timing",
-            "dgdiff_get_stats", "dgdiff_reset_stats", "dgdiff_mixture", "dgdiff_centre_weights"]
+            "dgdiff_get_stats", "dgdiff_reset_stats", "dgdiff_mixture", "dgdiff_centre_weights",
+            "dgdiff_absorb_table"]
 
 
 class dgdiff_opts(ctypes.Structure):
@@ -72,11 +73,14 @@ def _load():
     L.dgdiff_set_timing.argtypes = [H, i32]
     L.dgdiff_get_stats.argtypes = [H, ctypes.POINTER(dgdiff_stats_t)]
     L.dgdiff_reset_stats.argtypes = [H]
-    L.dgdiff_mixture.argtypes = [H, dp, dp]
-    L.dgdiff_centre_weights.argtypes = [i32, dp]
+    for name, args in (("dgdiff_mixture", [H, dp, dp]), ("dgdiff_centre_weights", [i32, dp]),
+                       ("dgdiff_absorb_table", [i32, dp])):
+        if hasattr(L, name):
+            getattr(L, name).argtypes = args
+            getattr(L, name).restype = ctypes.c_int
     for f in ("dgdiff_create", "dgdiff_solve_batch", "dgdiff_covariance", "dgdiff_source_moments",
               "dgdiff_get_density", "dgdiff_operator_table", "dgdiff_set_timing", "dgdiff_get_stats",
-              "dgdiff_reset_stats", "dgdiff_mixture", "dgdiff_centre_weights"):
+              "dgdiff_reset_stats"):
         getattr(L, f).restype = ctypes.c_int
     return L
 
@@ -168,6 +172,13 @@ def dgdiff_mixture(handle, R):
     res = np.zeros(1)
     _check(lib.dgdiff_mixture(handle, _dp(grid), _dp(res)))
     return grid, float(res[0])
+
+
+def dgdiff_absorb_table(degree):
+    d2 = 2 * ndof(degree)
+    A = np.zeros((16, 16, 5, d2, d2))
+    _check(lib.dgdiff_absorb_table(int(degree), _dp(A)))
+    return A
 
 
 def dgdiff_centre_weights(degree):

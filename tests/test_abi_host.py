@@ -133,6 +133,50 @@ def test_table_reproduces_oracle_operator(dg, p, orc):
         assert abs(mass_rate) < 1e-11 * np.abs(got).sum()
 
 
+def composite_apply_absorb(A, Aabs, mask, u):
+    """K0 tables applied pixel by pixel under ABSORB (test helper)."""
+    ny, nx = mask.shape
+    out = np.zeros_like(u)
+    offs = [(1, 0), (-1, 0), (0, 1), (0, -1)]
+    for j in range(ny):
+        for i in range(nx):
+            if mask[j, i]:
+                continue
+            code = outer = 0
+            nb = []
+            for bit, (di, dj) in enumerate(offs):
+                ii, jj = i + di, j + dj
+                if not (0 <= ii < nx and 0 <= jj < ny):
+                    outer |= 1 << bit
+                elif not mask[jj, ii]:
+                    code |= 1 << bit
+                    nb.append((bit + 1, ii, jj))
+            B = A[code] if outer == 0 else Aabs[code, outer]
+            acc = B[0] @ u[j, i].reshape(-1)
+            for o, ii, jj in nb:
+                acc += B[o] @ u[jj, ii].reshape(-1)
+            out[j, i] = acc.reshape(u.shape[2:])
+    return out
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_absorb_table_reproduces_oracle_operator(dg, p, orc):
+    """ABSORB (Eq. (4)): K0's boundary-pixel blocks + the interior table equal
+    O1's L(u) with outer_bc=1 on random masks touching every grid edge."""
+    A, _, _ = dg.dgdiff_operator_table(p)
+    Aabs = dg.dgdiff_absorb_table(p)
+    rng = np.random.default_rng(60 + p)
+    d = (p + 1) * (p + 2) // 2
+    for _ in range(3):
+        mask = (rng.random((9, 10)) < 0.3).astype(np.uint8)
+        u = rng.standard_normal((9, 10, 2, d))
+        u[mask.astype(bool)] = 0
+        h, D = 0.7, 1.9
+        ref = orc.apply_L(p, h, D, mask, u, outer_bc=1) * h * h / D
+        got = composite_apply_absorb(A, Aabs, mask, u)
+        assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
 def test_dt_max_and_shard(dg):
     assert abs(dg.dgdiff_dt_max(1, 1.0, 1.0) - 2.5127453 / 60) < 1e-15
     assert abs(dg.dgdiff_dt_max(1, 0.5, 2.0) - 2.5127453 / 60 * 0.125) < 1e-15
@@ -162,5 +206,5 @@ def test_argument_errors_are_reported(dg):
         dg.dgdiff_create(np.zeros((4, 4), np.uint8), -1.0, 1.0, 1)
     assert e.value.status == dg.E_ARG
     with pytest.raises(dg.DGDiffError) as e:
-        dg.dgdiff_create(np.zeros((4, 4), np.uint8), 1.0, 1.0, 1, dg.dgdiff_opts_default(outer_bc=1))
+        dg.dgdiff_create(np.zeros((4, 4), np.uint8), 1.0, 1.0, 1, dg.dgdiff_opts_default(outer_bc=2))
     assert e.value.status == dg.E_ARG

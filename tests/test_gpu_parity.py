@@ -336,3 +336,51 @@ def test_nccl_one_rank_world(dg, cfg):
             out.append((S, mu, g, res))
     for a, b in zip(out[0], out[1]):
         assert np.array_equal(a, b)
+
+
+# ---------------------------------------------------------------- ABSORB outer boundary (Eq. (4))
+@pytest.mark.parametrize("prec", [64, 32])
+def test_absorb_c1_golden_and_oracle(dg, orc, cfg, prec):
+    """outer_bc = ABSORB (Eq. (4)) on c1: densities vs O1 and the
+    independent implementation's m00 / Sigma after 200 steps."""
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "c1_independent_A10.json")))["absorb_200"]
+    m = cfg.mask("c1")
+    src = cfg.sources("c1")
+    ref_m, ref_d = orc.solve(1, 1.0, 1.0, m, src, 1 / 32, 200, outer_bc=1, keep_density=True)
+    with dg.Solver(m, 1.0, 1.0, 1, precision=prec, outer_bc=1, keep_density=1) as s:
+        s.solve(src, 1 / 32, 200)
+        S, _ = s.covariance()
+        mom = s.moments()
+        dens = s.density(0)
+    t = TOL[prec]
+    assert rel_l2(dens, ref_d[0]) <= t["dens"]
+    assert abs(mom[0, 0] - g["m00"]) <= (1e-12 if prec == 64 else 1e-5)
+    assert np.allclose([S[0, 0], S[0, 1], S[1, 1]], g["sigma"], rtol=t["sig"], atol=t["sig"])
+
+
+@pytest.mark.parametrize("p,prec", [(1, 64), (1, 32), (2, 64)])
+def test_absorb_random_masks(dg, orc, p, prec):
+    """ABSORB on random masks touching every grid edge (all (code, outer)
+    combinations occur), ragged two-chunk batch, vs O1."""
+    rng = np.random.default_rng(700 + p * 3 + prec)
+    mk = (rng.random((21, 26)) < 0.3).astype(np.uint8)
+    free = np.argwhere(mk == 0)
+    G = 64 if p == 1 and prec == 64 else (128 if p == 1 else 32)
+    n = G + 7
+    pick = free[rng.integers(0, len(free), n)]
+    src = np.stack([pick[:, 1], pick[:, 0]], 1).astype(np.int32)
+    dt = 1 / 32 if p == 1 else 1 / 128
+    ref_m, ref_d = orc.solve(p, 1.0, 1.0, mk, src, dt, 80, outer_bc=1, keep_density=True)
+    with dg.Solver(mk, 1.0, 1.0, p, precision=prec, outer_bc=1, keep_density=1, max_chunk=G) as s:
+        s.solve(src, dt, 80)
+        S, _ = s.covariance()
+        mom = s.moments()
+        dens = [s.density(k) for k in range(G, n)]
+    t = TOL[prec]
+    for k, dk in zip(range(G, n), dens):
+        assert rel_l2(dk, ref_d[k]) <= t["dens"], k
+    assert mom_err(mom, ref_m) <= t["mom"]
+    assert sig_err(S, orc.sigma(ref_m)[0]) <= t["sig"]
+    assert mom[:, 0].min() < 1.0                                  # mass leaves through the outer square
