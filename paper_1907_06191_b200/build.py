@@ -1,8 +1,10 @@
 """Build the in-tree native libraries of the product path.
 
-  libdgdiff.so  -- csrc/dgdiff.cu + csrc/operator.cpp, nvcc for sm_100a
-                   (-gencode arch=compute_100a,code=sm_100a -lineinfo), static
-                   cudart, NCCL dlopen'ed at run time
+  libdgdiff.so  -- csrc/*.cu translation units + csrc/operator.cpp, compiled in
+                   parallel by nvcc for sm_100a (-gencode arch=compute_100a,
+                   code=sm_100a -lineinfo), static cudart, NCCL dlopen'ed at
+                   run time; csrc/tables.inc is generated first by gen_tables
+                   (K0 at build time)
   librsa.so     -- csrc/rsa.c (input generation helper, gcc)
 """
 from __future__ import annotations

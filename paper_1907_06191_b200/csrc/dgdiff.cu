@@ -2,9 +2,9 @@
 // hot path of arXiv 1907.06191 (PAPER.md, cited P:<line>).
 //
 //   K1 k_init      Dirac Cauchy data for a chunk of sources
-//   K2 k_stage     one SSP-RK3 stage of the DG operator (Eq. (7))
+//   K2 k_stage_ring one SSP-RK3 stage of the DG operator (Eq. (7))
 //                  as a 5-point composite stencil over extracellular pixels
-//   K3 k_stage_tb  (temporal blocking, see stage_tb.cuh)
+//   K3 k_step_fused (temporal blocking, opt-in; step_fused.cuh)
 //   K4 k_moments   m00 m10 m01 m20 m11 m02 per source
 //   K5 k_finalize  mixture mean and covariance Sigma; preceded by
 //                  one ncclAllReduce of the moment table when nranks > 1

@@ -384,3 +384,64 @@ def test_absorb_random_masks(dg, orc, p, prec):
     assert mom_err(mom, ref_m) <= t["mom"]
     assert sig_err(S, orc.sigma(ref_m)[0]) <= t["sig"]
     assert mom[:, 0].min() < 1.0                                  # mass leaves through the outer square
+
+
+# ---------------------------------------------------------------- edge cases
+def test_zero_steps_is_projected_dirac(dg, cfg):
+    """nsteps = 0: moments of the projected Dirac itself, P1 Sigma(0) =
+    h^2 [[1/20, 1/10], [1/10, 1/20]] (closed form) and mass 1."""
+    m = np.zeros((9, 9), np.uint8)
+    with dg.Solver(m, 0.5, 1.0, 1) as s:
+        s.solve([[4, 4], [2, 6]], 0.001, 0)
+        S, mu = s.covariance(0.0)
+        mom = s.moments()
+    assert np.allclose(mom[:, 0], 1.0, atol=1e-14)
+    assert np.allclose(S, 0.25 * np.array([[1 / 20, 1 / 10], [1 / 10, 1 / 20]]), atol=1e-15)
+    assert np.allclose(mu, 0, atol=1e-15)
+
+
+@pytest.mark.parametrize("prec", [64, 32])
+def test_trapped_pocket_and_enclosure(dg, orc, prec):
+    """A source in a one-pixel pocket never leaves it (all four faces closed:
+    its operator is the code-0 block) and keeps mass 1; a source inside a
+    closed 5x5 room of axons conserves mass and matches O1."""
+    m = np.ones((16, 16), np.uint8)
+    m[3, 3] = 0                                   # isolated pixel
+    m[8:13, 6:11] = 0                             # closed room
+    src = np.array([[3, 3], [8, 10], [6, 12]], np.int32)
+    ref_m, ref_d = orc.solve(1, 1.0, 1.0, m, src, 1 / 32, 300, keep_density=True)
+    with dg.Solver(m, 1.0, 1.0, 1, precision=prec, keep_density=1) as s:
+        s.solve(src, 1 / 32, 300)
+        mom = s.moments()
+        d = [s.density(k) for k in range(3)]
+    t = TOL[prec]
+    for k in range(3):
+        assert rel_l2(d[k], ref_d[k]) <= t["dens"]
+    assert np.abs(mom[:, 0] - 1).max() <= (1e-12 if prec == 64 else 2e-6)
+    assert np.abs(d[0]).sum() == np.abs(d[0][3, 3]).sum()    # nothing outside the pocket
+
+
+def test_argument_and_state_errors(dg, cfg):
+    m = cfg.mask("c1")
+    with pytest.raises(dg.DGDiffError) as e:
+        dg.Solver(m, 1.0, 1.0, 1).solve(np.zeros((0, 2), np.int32), 1 / 32, 1)
+    assert e.value.status == dg.E_ARG
+    with dg.Solver(m, 1.0, 1.0, 1) as s:
+        s.solve([[4, 16]], 1 / 32, 2)
+        with pytest.raises(dg.DGDiffError) as e:
+            s.density(0)                                          # keep_density off
+        assert e.value.status == dg.E_STATE
+        with pytest.raises(dg.DGDiffError) as e:
+            s.mixture()                                           # mixture_radius 0
+        assert e.value.status == dg.E_STATE
+        with pytest.raises(dg.DGDiffError) as e:
+            s.solve([[-1, 3]], 1 / 32, 1)
+        assert e.value.status == dg.E_SOURCE
+    dtm = dg.dgdiff_dt_max(1, 1.0, 1.0)
+    with dg.Solver(m, 1.0, 1.0, 1) as s:
+        s.solve([[4, 16]], dtm, 10)                               # the limit itself is allowed
+        S, _ = s.covariance()
+        assert np.all(np.isfinite(S))
+    with pytest.raises(dg.DGDiffError) as e:
+        dg.Solver(m, 1.0, 1.0, 1, outer_bc=1, temporal_steps=2)
+    assert e.value.status == dg.E_ARG
