@@ -132,6 +132,20 @@ dgdiff_status dgdiff_covariance(dgdiff_t, double delta, double sigma[4], double 
  * When nranks > 1 the grid is all-reduced (NCCL) first.  Synchronises. */
 dgdiff_status dgdiff_mixture(dgdiff_t, double *grid, double *residual);
 
+/* Monte-Carlo cross-check (the paper's MC comparison): K walkers
+ * per source start at the source pixel centres and take nsteps steps of
+ * length l = sqrt(4 D delta / nsteps) in uniform directions; a step
+ * whose segment enters an axon pixel or leaves the grid is rejected (the
+ * walker stays).  Needs l < h (nsteps >= 4 D delta / h^2) -> else E_ARG.
+ * Philox4x32-10 counter-based randomness keyed by (seed, walker): runs are
+ * reproducible.  Walker w belongs to source w mod n.  sigma[4] (row-major,
+ * symmetric) and mu[2] of the pooled displacements, se[3] the standard errors
+ * of sxx, sxy, syy from 32 batches of walkers (each batch spans all sources);
+ * disp (nullable) [n*K][2] the displacements in pixel units.  Synchronises. */
+dgdiff_status dgdiff_mc_covariance(dgdiff_t, const int32_t *sources, int64_t n, int32_t walkers_per_source,
+                                   int64_t nsteps, double delta, uint32_t seed, double sigma[4], double mu[2],
+                                   double se[3], double *disp);
+
 /* Per-source moments [n][6] = m00 m10 m01 m20 m11 m02 of the last solve,
  * about each source point; rows of other ranks' shards are zero until
  * dgdiff_covariance has run.  Synchronises. */

@@ -26,6 +26,7 @@
 #include "kernels.cuh"
 #include "operator.h"
 #include "launch.h"
+#include "mc_walk.cuh"
 #include "stage_imm.cuh"  // compile-time operator (tab<P>) for the create-time check
 
 using namespace dgk;
@@ -1098,6 +1099,57 @@ extern "C" dgdiff_status dgdiff_mixture(dgdiff_t H, double *grid, double *residu
   CK(cudaMemcpyAsync(&res, H->d_mix_out + nc, sizeof(double), cudaMemcpyDeviceToHost, H->stream));
   CK(cudaStreamSynchronize(H->stream));
   if (residual) *residual = res;
+  return DGDIFF_OK;
+}
+
+extern "C" dgdiff_status dgdiff_mc_covariance(dgdiff_t H, const int32_t *sources, int64_t n,
+                                              int32_t walkers_per_source, int64_t nsteps, double delta,
+                                              uint32_t seed, double sigma[4], double mu[2], double se[3],
+                                              double *disp) {
+  if (!H || !sources || !sigma) return fail(DGDIFF_E_ARG, "NULL argument");
+  if (n < 1 || walkers_per_source < 1 || nsteps < 1 || !(delta > 0))
+    return fail(DGDIFF_E_ARG, "need n, walkers_per_source, nsteps >= 1 and delta > 0");
+  const int64_t nwalk = n * (int64_t)walkers_per_source;
+  if (nwalk >= (1LL << 32)) return fail(DGDIFF_E_ARG, "too many walkers");
+  const double l = sqrt(4.0 * H->D * delta / (double)nsteps) / H->h;   // P:318, in pixels
+  if (!(l < 1.0)) return fail(DGDIFF_E_ARG, "step length %.4g h >= h: use nsteps >= 4 D delta / h^2", l);
+  for (int64_t s = 0; s < n; s++) {
+    int i = sources[2 * s], j = sources[2 * s + 1];
+    if (i < 0 || j < 0 || i >= H->nx || j >= H->ny || H->h_aidx[(size_t)j * H->nx + i] < 0)
+      return fail(DGDIFF_E_SOURCE, "source %lld (%d,%d) is outside the grid or on an axon pixel", (long long)s, i, j);
+  }
+  CK(cudaSetDevice(H->dev));
+  int32_t *d_src = nullptr;
+  double *d_part = nullptr, *d_disp = nullptr, *d_res = nullptr;
+  const int blocks = (int)((nwalk + 255) / 256);
+  dgdiff_status st = DGDIFF_OK;
+  auto cleanup = [&]() { cudaFree(d_src); cudaFree(d_part); cudaFree(d_disp); cudaFree(d_res); };
+  cudaError_t e = cudaMalloc(&d_src, sizeof(int32_t) * 2 * n);
+  if (e == cudaSuccess) e = cudaMalloc(&d_part, sizeof(double) * 5 * blocks);
+  if (e == cudaSuccess) e = cudaMalloc(&d_res, sizeof(double) * 8);
+  if (e == cudaSuccess && disp) e = cudaMalloc(&d_disp, sizeof(double) * 2 * nwalk);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_src, sources, sizeof(int32_t) * 2 * n, cudaMemcpyHostToDevice, H->stream);
+  if (e == cudaSuccess) {
+    dgk::k_mc_walk<<<blocks, 256, 0, H->stream>>>(H->d_aidx, H->nx, H->ny, d_src, nwalk, n, nsteps, l, seed,
+                                                  d_part, d_disp);
+    dgk::k_mc_final<<<1, 32, 0, H->stream>>>(d_part, blocks, nwalk, std::min(32, blocks), H->h, d_res);
+    H->st.launches += 2;
+    e = cudaGetLastError();
+  }
+  double out[8];
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out, d_res, sizeof out, cudaMemcpyDeviceToHost, H->stream);
+  if (e == cudaSuccess && disp)
+    e = cudaMemcpyAsync(disp, d_disp, sizeof(double) * 2 * nwalk, cudaMemcpyDeviceToHost, H->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(H->stream);
+  if (e != cudaSuccess) st = fail(DGDIFF_E_CUDA, "mc: %s", cudaGetErrorString(e));
+  cleanup();
+  if (st != DGDIFF_OK) return st;
+  sigma[0] = out[0];
+  sigma[1] = out[1];
+  sigma[2] = out[1];
+  sigma[3] = out[2];
+  if (mu) { mu[0] = out[3]; mu[1] = out[4]; }
+  if (se) { se[0] = out[5]; se[1] = out[6]; se[2] = out[7]; }
   return DGDIFF_OK;
 }
 

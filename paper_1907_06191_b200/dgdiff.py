@@ -22,7 +22,7 @@ EXPORTED = ["dgdiff_opts_default", "dgdiff_create", "dgdiff_solve_batch", "dgdif
             "dgdiff_source_moments", "dgdiff_get_density", "dgdiff_dt_max", "dgdiff_last_error",
             "dgdiff_destroy", "dgdiff_operator_table", "dgdiff_shard", "dgdiff_set_timing",
             "dgdiff_get_stats", "dgdiff_reset_stats", "dgdiff_mixture", "dgdiff_centre_weights",
-            "dgdiff_absorb_table"]
+            "dgdiff_absorb_table", "dgdiff_mc_covariance"]
 
 
 class dgdiff_opts(ctypes.Structure):
@@ -74,7 +74,9 @@ def _load():
     L.dgdiff_get_stats.argtypes = [H, ctypes.POINTER(dgdiff_stats_t)]
     L.dgdiff_reset_stats.argtypes = [H]
     for name, args in (("dgdiff_mixture", [H, dp, dp]), ("dgdiff_centre_weights", [i32, dp]),
-                       ("dgdiff_absorb_table", [i32, dp])):
+                       ("dgdiff_absorb_table", [i32, dp]),
+                       ("dgdiff_mc_covariance", [H, ctypes.POINTER(ctypes.c_int32), i64, i32, i64, dbl,
+                                                 ctypes.c_uint32, dp, dp, dp, dp])):
         if hasattr(L, name):
             getattr(L, name).argtypes = args
             getattr(L, name).restype = ctypes.c_int
@@ -174,6 +176,18 @@ def dgdiff_mixture(handle, R):
     return grid, float(res[0])
 
 
+def dgdiff_mc_covariance(handle, sources, walkers_per_source, nsteps, delta, seed=1, want_disp=False):
+    src = np.ascontiguousarray(sources, dtype=np.int32).reshape(-1, 2)
+    S = np.zeros(4)
+    mu = np.zeros(2)
+    se = np.zeros(3)
+    disp = np.zeros((src.shape[0] * walkers_per_source, 2)) if want_disp else None
+    _check(lib.dgdiff_mc_covariance(handle, src.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), src.shape[0],
+                                    int(walkers_per_source), int(nsteps), float(delta), int(seed) & 0xFFFFFFFF,
+                                    _dp(S), _dp(mu), _dp(se), _dp(disp) if disp is not None else None))
+    return (S.reshape(2, 2), mu, se, disp) if want_disp else (S.reshape(2, 2), mu, se)
+
+
 def dgdiff_absorb_table(degree):
     d2 = 2 * ndof(degree)
     A = np.zeros((16, 16, 5, d2, d2))
@@ -234,6 +248,10 @@ class Solver:
     def mixture(self):
         """(grid [(2R+1)][(2R+1)], Eq. (9) residual); needs mixture_radius=R."""
         return dgdiff_mixture(self.handle, self.opts.mixture_radius)
+
+    def mc_covariance(self, sources, walkers_per_source, nsteps, delta, seed=1, want_disp=False):
+        """Monte-Carlo cross-check of Sigma on this substrate."""
+        return dgdiff_mc_covariance(self.handle, sources, walkers_per_source, nsteps, delta, seed, want_disp)
 
     def density(self, src):
         return dgdiff_get_density(self.handle, src, self.nx, self.ny, self.degree)

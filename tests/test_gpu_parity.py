@@ -445,3 +445,52 @@ def test_argument_and_state_errors(dg, cfg):
     with pytest.raises(dg.DGDiffError) as e:
         dg.Solver(m, 1.0, 1.0, 1, outer_bc=1, temporal_steps=2)
     assert e.value.status == dg.E_ARG
+
+
+# ---------------------------------------------------------------- N3 Monte-Carlo cross-check
+def test_mc_matches_reference_bitwise(dg):
+    """GPU walkers == the numpy reference (same Philox stream, same rules):
+    displacements bit for bit on a random mask with walls."""
+    from oracle import mc
+    rng = np.random.default_rng(17)
+    m = (rng.random((24, 24)) < 0.35).astype(np.uint8)
+    free = np.argwhere(m[6:18, 6:18] == 0) + 6
+    src = np.stack([free[:5, 1], free[:5, 0]], 1).astype(np.int32)
+    K, T, delta = 40, 150, 3.0
+    with dg.Solver(m, 1.0, 1.0, 1) as s:
+        S, mu, se, disp = s.mc_covariance(src, K, T, delta, seed=99, want_disp=True)
+    l = np.sqrt(4 * 1.0 * delta / T)
+    ref = mc.walk(m, src, K, T, l, 99)
+    assert np.array_equal(disp, ref)
+
+
+def test_mc_free_space_sigma(dg):
+    """Free space: MC Sigma = 2 D Delta I within 4 standard errors (2D walk of
+    step l: E[dx^2] = T l^2 / 2 = 2 D Delta)."""
+    m = np.zeros((256, 256), np.uint8)
+    src = np.array([[128, 128], [120, 131]], np.int32)
+    with dg.Solver(m, 0.5, 2.0, 1) as s:
+        S, mu, se = s.mc_covariance(src, 200000, 400, 1.5, seed=5)
+    want = 2 * 2.0 * 1.5
+    assert abs(S[0, 0] - want) < 4 * se[0] and abs(S[1, 1] - want) < 4 * se[2]
+    assert abs(S[0, 1]) < 4 * se[1]
+
+
+@pytest.mark.parametrize("p,tol", [(2, 0.03), (1, 0.08)])
+def test_dg_vs_mc_gamma_substrate(dg, cfg, p, tol):
+    """Physics cross-check (the paper's DG-vs-MC comparison) on the
+    c3 Gamma substrate, 64 sources, Delta = 8: MC with reflecting (rejecting)
+    walls on the same pixel mask vs DG.  Measured: P2 within ~1.2 %, P1 ~5 %
+    low (the u+ = 0 wall flux of the paper's scheme, reading R6, is an O(h)
+    wall error); both hindered well below 2 D Delta."""
+    m = cfg.mask("c3")
+    src = cfg.sources("c3", 64)
+    dt = 1 / 32 if p == 1 else 1 / 128
+    nsteps = int(round(8.0 / dt))
+    with dg.Solver(m, 1.0, 1.0, p) as s:
+        s.solve(src, dt, nsteps)
+        S, _ = s.covariance()
+        Sm, _, se = s.mc_covariance(src, 20000, 4096, 8.0, seed=77)
+    for k in (0, 1):
+        assert abs(S[k, k] - Sm[k, k]) <= tol * Sm[k, k] + 4 * se[2 * k]
+        assert S[k, k] < 0.7 * 16.0 and Sm[k, k] < 0.7 * 16.0
