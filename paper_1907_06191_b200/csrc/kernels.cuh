@@ -12,6 +12,7 @@
 // kernels (v1, v2), 8-byte lanes for the row-ring kernel (v3), so that a
 // P1 pixel is 1.5 KB and four full row tiles fit in shared memory.
 #pragma once
+#include <type_traits>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -37,6 +38,24 @@ __device__ __forceinline__ V pack(const T (&x)[NV]) {
   else if constexpr (NV == 2) { v.x = x[0]; v.y = x[1]; }
   else { v.x = x[0]; v.y = x[1]; v.z = x[2]; v.w = x[3]; }
   return v;
+}
+
+// acc[e] += a * x[e] for the NV sources of one lane.  fp32 pairs go through
+// packed FFMA2 (fma.rn.f32x2 with a broadcast coefficient: two independent
+// round-to-nearest FMAs, bit-identical to scalar fmaf, half the issue slots).
+template <typename T, int NV>
+__device__ __forceinline__ void fma_bc(T a, const T (&x)[NV], T (&acc)[NV]) {
+  if constexpr (std::is_same<T, float>::value && NV % 2 == 0) {
+#pragma unroll
+    for (int e = 0; e < NV; e += 2) {
+      const float2 r = __ffma2_rn(make_float2(a, a), make_float2(x[e], x[e + 1]), make_float2(acc[e], acc[e + 1]));
+      acc[e] = r.x;
+      acc[e + 1] = r.y;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < NV; e++) acc[e] = fma(a, x[e], acc[e]);
+  }
 }
 
 // read-only-path load (state of the previous stage, never written in-kernel)

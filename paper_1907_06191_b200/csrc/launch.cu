@@ -6,8 +6,12 @@
 namespace dgl {
 
 int ring_width(int P, bool alpha) {
-  if (P == 1) return alpha ? dgk::RingCfg<1, 16, true>::W : dgk::RingCfg<1, 16, false>::W;
-  return alpha ? dgk::RingCfg<2, 8, true>::W : dgk::RingCfg<2, 8, false>::W;
+  if (P == 1) {
+    const bool r2u = alpha && !dgk::ring_u0_direct<1>();
+    return r2u ? dgk::RingCfg<1, 16, true>::W : dgk::RingCfg<1, 16, false>::W;
+  }
+  const bool r2u = alpha && !dgk::ring_u0_direct<2>();
+  return r2u ? dgk::RingCfg<2, 8, true>::W : dgk::RingCfg<2, 8, false>::W;
 }
 
 cudaError_t launch_stage(int which, int prec, int P, bool alpha, const StageArgs &a) {

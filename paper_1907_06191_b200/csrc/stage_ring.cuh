@@ -13,14 +13,14 @@
 //       batches of up to 32 rows (one per lane): wait until the ring slots are
 //       released (empty barriers), write the row's metadata, arm full[r] with
 //       the byte count and issue the bulk copies: U_in tile [h0, h1) into
-//       ring 1, and -- for rows that are computed -- the u0 tile [c0, c1)
-//       (alpha stages) into ring 2 and the neighbour indices nbr[c0, c1).
+//       ring 1, and -- for rows that are computed -- the neighbour indices
+//       nbr[c0, c1) (and, staged variant only, the u0 tile) into ring 2.
 //   consumer warps           the band's computed pixels, dealt out round-robin
 //       in raster order (warp w: pixels w, w+NC, ...): for a pixel of row j,
 //       wait full[j-1..j+1]; apply the 5-point composite operator with
 //       compile-time immediates (stage_imm.cuh) from shared memory, add the
-//       RK combination with u0 from ring 2, store to HBM; release rows whose
-//       last reader has passed.
+//       RK combination with u0 (alpha stages: loaded from HBM at the start of
+//       the pixel), store to HBM; release rows whose last reader has passed.
 //
 // No CTA-wide barrier: warps drift within the ring, the producer keeps as many
 // rows in flight as the rings hold (adaptive lookahead: Gamma rows are ~40 %
@@ -43,6 +43,17 @@ constexpr int RING_Q = 16;         // row entries (full/empty barrier pairs)
 #define RING_N1_NOALPHA(W, PXB, budget) ((budget) / (PXB))
 #endif
 constexpr int RING_MAXBAND = 256;  // max rows per band (+2 halo rows)
+// alpha stages: u0 is read by the consumer straight from HBM (issued before
+// the pixel's MACs, so its latency hides behind them) instead of being staged
+// in ring 2; the freed shared memory buys the stage-1 geometry (W = 16 for
+// P1, deeper ring 1).  P2 keeps the staged variant (16 consumer warps at 96
+// registers: the extra u0 registers would spill).  -DDGDIFF_U0_RING restores
+// the staged variant everywhere.
+#ifdef DGDIFF_U0_RING
+template <int P> constexpr bool ring_u0_direct() { return false; }
+#else
+template <int P> constexpr bool ring_u0_direct() { return P == 1; }
+#endif
 
 // strip width W and consumer warps NC per (degree, lane bytes, alpha term): a
 // pixel tile is 2d x 32 lanes x lane bytes; four full halo'd rows must fit in
@@ -58,17 +69,18 @@ template <typename T, int NV, int P, bool ALPHA>
 struct RingGeom {
   static constexpr int G = 32 * NV;
   static constexpr int D2 = (P + 1) * (P + 2);
-  static constexpr int W = RingCfg<P, NV * (int)sizeof(T), ALPHA>::W;
-  static constexpr int NC = RingCfg<P, NV * (int)sizeof(T), ALPHA>::NC;
+  static constexpr bool R2U = ALPHA && !ring_u0_direct<P>();   // u0 tiles staged in ring 2
+  static constexpr int W = RingCfg<P, NV * (int)sizeof(T), R2U>::W;
+  static constexpr int NC = RingCfg<P, NV * (int)sizeof(T), R2U>::NC;
   static constexpr int PXB = D2 * G * (int)sizeof(T);  // one pixel tile (one group)
   static constexpr int SMEM_MAX = 232448;
   static constexpr int EXTRA = 2 * RING_Q * 8 + RING_Q * 32 + (RING_MAXBAND + 2) * 16 + 2 * RING_Q * 4;
-  // ring 2 holds u0 tiles (alpha stages) and neighbour indices; without the
-  // alpha term it only holds the 16-byte indices and ring 1 takes the rest
-  static constexpr int N2 = ALPHA ? 4 * W : 16 * W;
-  static constexpr int N1 = ALPHA ? 4 * (W + 2) : RING_N1_NOALPHA(W, PXB, SMEM_MAX - EXTRA - N2 * 16);
+  // ring 2 holds staged u0 tiles (R2U) and neighbour indices; otherwise it
+  // only holds the 16-byte indices and ring 1 takes the rest
+  static constexpr int N2 = R2U ? 4 * W : 16 * W;
+  static constexpr int N1 = R2U ? 4 * (W + 2) : RING_N1_NOALPHA(W, PXB, SMEM_MAX - EXTRA - N2 * 16);
   static constexpr int OFF_R2 = N1 * PXB;
-  static constexpr int OFF_NB = OFF_R2 + (ALPHA ? N2 * PXB : 0);
+  static constexpr int OFF_NB = OFF_R2 + (R2U ? N2 * PXB : 0);
   static constexpr int OFF_BAR = OFF_NB + N2 * 16;
   static constexpr int OFF_META = OFF_BAR + 2 * RING_Q * 8;
   static constexpr int OFF_RT = OFF_META + RING_Q * 32;
@@ -176,7 +188,7 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
           meta[q] = m;
           rv[q] = v1 + e1;
           rv[Q + q] = v2 + e2;
-          const uint32_t bytes = n1 * PXB + (HAS_ALPHA ? n2 * PXB : 0u) + n2 * 16u;
+          const uint32_t bytes = n1 * PXB + (Gm::R2U ? n2 * PXB : 0u) + n2 * 16u;
           mbar_expect_tx(&full[q], bytes);
           if (n1) {
             const uint32_t a1 = min(n1, (uint32_t)Gm::N1 - p1);
@@ -186,7 +198,7 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
           }
           if (n2) {
             const uint32_t a2 = min(n2, (uint32_t)Gm::N2 - p2);
-            if (HAS_ALPHA) {
+            if (Gm::R2U) {
               const T *src = U0g + (size_t)t.y * D2 * G;
               bulk_g2s(ring2 + (size_t)p2 * PXB, src, a2 * PXB, &full[q]);
               if (n2 > a2) bulk_g2s(ring2, src + (size_t)a2 * D2 * G, (n2 - a2) * PXB, &full[q]);
@@ -218,6 +230,7 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
     const int jb0 = b * band_rows, jb1 = min(ny, jb0 + band_rows);
     const int lo = max(0, jb0 - 1), hi = min(ny - 1, jb1);
     T *Uog = Uout + g * gstride + lane * NV;
+    const T *U0l = U0 + g * gstride + lane * NV;
     auto seq = [&](int r) { return Lbase + (uint32_t)(r - lo); };
     auto wait_row = [&](int r) {
       if (r >= lo && r <= hi) {
@@ -258,7 +271,13 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
       if (sl2 >= Gm::N2) sl2 -= Gm::N2;
       const int4 nb = nbr_ring[sl2];
       const T *ps = tile1(mc, a);
-      T xs[D2][NV], acc[D2][NV], xn[D2][NV];
+      T xs[D2][NV], acc[D2][NV], xn[D2][NV], z[D2][NV];
+      if constexpr (HAS_ALPHA && !Gm::R2U) {
+        // u0 straight from HBM (coherent load: stage 3 writes u in place; this
+        // lane reads its elements before it writes them)
+#pragma unroll
+        for (int k = 0; k < D2; k++) ldvc<T, NV>(U0l + ((size_t)a * D2 + k) * G, z[k]);
+      }
 #pragma unroll
       for (int k = 0; k < D2; k++) lds<T, NV>(ps + k * G, xs[k]);
 #pragma unroll
@@ -318,10 +337,9 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
       for (int k = 0; k < D2; k++) {
         T y[NV];
         if (HAS_ALPHA) {
-          T z[NV];
-          lds<T, NV>(pu + k * G, z);
+          if constexpr (Gm::R2U) lds<T, NV>(pu + k * G, z[k]);
 #pragma unroll
-          for (int e = 0; e < NV; e++) y[e] = xs[k][e] + alpha * (z[e] - xs[k][e]) + cs * acc[k][e];
+          for (int e = 0; e < NV; e++) y[e] = xs[k][e] + alpha * (z[k][e] - xs[k][e]) + cs * acc[k][e];
         } else {
 #pragma unroll
           for (int e = 0; e < NV; e++) y[e] = xs[k][e] + cs * acc[k][e];
@@ -368,7 +386,7 @@ cudaError_t launch_ring(const dgl::StageArgs &a) {
       ALPHA ? a.nstrips : a.nstrips_na, a.ngroups,
       band_rows, nitems, (T)a.alpha, (T)a.cs, a.diag,
       std::max(4, std::min(RING_Q - 1, alpha_max_ahead(a, ALPHA))),
-      ALPHA ? Gm::N1 : std::max(4 * (Gm::W + 2), std::min(Gm::N1, a.n1_use_na > 0 ? a.n1_use_na : Gm::N1)),
+      Gm::R2U ? Gm::N1 : std::max(4 * (Gm::W + 2), std::min(Gm::N1, a.n1_use_na > 0 ? a.n1_use_na : Gm::N1)),
       std::max(4 * Gm::W, std::min(Gm::N2, a.n2_use > 0 ? a.n2_use : Gm::N2)), (const T *)a.Aabs);
   return cudaGetLastError();
 }
