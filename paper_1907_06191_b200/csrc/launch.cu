@@ -6,12 +6,15 @@
 namespace dgl {
 
 int ring_width(int P, bool alpha) {
+  using namespace dgk;
   if (P == 1) {
-    const bool r2u = alpha && !dgk::ring_u0_direct<1>();
-    return r2u ? dgk::RingCfg<1, 16, true>::W : dgk::RingCfg<1, 16, false>::W;
+    const int m = ring_mode<1>(alpha);
+    return m == RING_PLAIN ? RingCfg<1, 16, RING_PLAIN>::W
+           : m == RING_U0_STAGED ? RingCfg<1, 16, RING_U0_STAGED>::W : RingCfg<1, 16, RING_U0_DIRECT>::W;
   }
-  const bool r2u = alpha && !dgk::ring_u0_direct<2>();
-  return r2u ? dgk::RingCfg<2, 8, true>::W : dgk::RingCfg<2, 8, false>::W;
+  const int m = ring_mode<2>(alpha);
+  return m == RING_PLAIN ? RingCfg<2, 8, RING_PLAIN>::W
+         : m == RING_U0_STAGED ? RingCfg<2, 8, RING_U0_STAGED>::W : RingCfg<2, 8, RING_U0_DIRECT>::W;
 }
 
 cudaError_t launch_stage(int which, int prec, int P, bool alpha, const StageArgs &a) {

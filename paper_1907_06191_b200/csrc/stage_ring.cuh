@@ -46,32 +46,38 @@ constexpr int RING_MAXBAND = 256;  // max rows per band (+2 halo rows)
 // alpha stages: u0 is read by the consumer straight from HBM (issued before
 // the pixel's MACs, so its latency hides behind them) instead of being staged
 // in ring 2; the freed shared memory buys the stage-1 geometry (W = 16 for
-// P1, deeper ring 1).  P2 keeps the staged variant (16 consumer warps at 96
-// registers: the extra u0 registers would spill).  -DDGDIFF_U0_RING restores
-// the staged variant everywhere.
+// P1, deeper ring 1).  -DDGDIFF_U0_RING restores the staged variant.
 #ifdef DGDIFF_U0_RING
 template <int P> constexpr bool ring_u0_direct() { return false; }
 #else
-template <int P> constexpr bool ring_u0_direct() { return P == 1; }
+template <int P> constexpr bool ring_u0_direct() { return true; }
 #endif
 
-// strip width W and consumer warps NC per (degree, lane bytes, alpha term): a
-// pixel tile is 2d x 32 lanes x lane bytes; four full halo'd rows must fit in
-// ring 1.  Without the alpha term ring 2 only holds neighbour indices, so the
-// P1 stage-1 kernel affords W = 16 (half the rows per byte of W = 8).
-template <int P, int LB, bool ALPHA> struct RingCfg;
-template <> struct RingCfg<1, 16, true> { static constexpr int W = 8, NC = 8; };   // NC swept 4/8/12/16
-template <> struct RingCfg<1, 16, false> { static constexpr int W = 16, NC = 8; };
-template <> struct RingCfg<2, 8, true> { static constexpr int W = 8, NC = 16; };
-template <> struct RingCfg<2, 8, false> { static constexpr int W = 8, NC = 16; };
+// strip width W and consumer warps NC per (degree, lane bytes, mode): a pixel
+// tile is 2d x 32 lanes x lane bytes; four full halo'd rows must fit in ring
+// 1.  Modes: RING_PLAIN (stage 1, no alpha term: ring 2 only holds neighbour
+// indices, so P1 affords W = 16, half the rows per byte of W = 8),
+// RING_U0_STAGED (u0 tiles in ring 2), RING_U0_DIRECT (u0 from HBM into
+// registers: P2 runs it with 12 consumer warps so the extra registers fit).
+enum { RING_PLAIN = 0, RING_U0_STAGED = 1, RING_U0_DIRECT = 2 };
+template <int P, int LB, int MODE> struct RingCfg;
+template <> struct RingCfg<1, 16, RING_PLAIN> { static constexpr int W = 16, NC = 8; };   // NC swept 4/8/12/16
+template <> struct RingCfg<1, 16, RING_U0_STAGED> { static constexpr int W = 8, NC = 8; };
+template <> struct RingCfg<1, 16, RING_U0_DIRECT> { static constexpr int W = 16, NC = 8; };
+template <> struct RingCfg<2, 8, RING_PLAIN> { static constexpr int W = 16, NC = 16; };   // c5: W 8 -> 16 -29 %
+template <> struct RingCfg<2, 8, RING_U0_STAGED> { static constexpr int W = 8, NC = 16; };
+template <> struct RingCfg<2, 8, RING_U0_DIRECT> { static constexpr int W = 16, NC = 12; };   // c5: NC 8 -> 12 -4 %
+template <int P> constexpr int ring_mode(bool alpha) {
+  return alpha ? (ring_u0_direct<P>() ? RING_U0_DIRECT : RING_U0_STAGED) : RING_PLAIN;
+}
 
 template <typename T, int NV, int P, bool ALPHA>
 struct RingGeom {
   static constexpr int G = 32 * NV;
   static constexpr int D2 = (P + 1) * (P + 2);
   static constexpr bool R2U = ALPHA && !ring_u0_direct<P>();   // u0 tiles staged in ring 2
-  static constexpr int W = RingCfg<P, NV * (int)sizeof(T), R2U>::W;
-  static constexpr int NC = RingCfg<P, NV * (int)sizeof(T), R2U>::NC;
+  static constexpr int W = RingCfg<P, NV * (int)sizeof(T), ring_mode<P>(ALPHA)>::W;
+  static constexpr int NC = RingCfg<P, NV * (int)sizeof(T), ring_mode<P>(ALPHA)>::NC;
   static constexpr int PXB = D2 * G * (int)sizeof(T);  // one pixel tile (one group)
   static constexpr int SMEM_MAX = 232448;
   static constexpr int EXTRA = 2 * RING_Q * 8 + RING_Q * 32 + (RING_MAXBAND + 2) * 16 + 2 * RING_Q * 4;
