@@ -77,11 +77,24 @@ typedef struct {
                              loads; 3 = v3, row-marching shared-memory ring fed
                              by bulk TMA.  Results agree to rounding; the
                              state layout (and so the source-group size) differs:
-                             v1/v2 16-byte lanes, v3 8-byte lanes */
+                             v1/v2 16-byte lanes; v3 16-byte lanes for P1,
+                             8-byte lanes for P2 */
   int32_t mixture_radius; /* R > 0: accumulate the mixture density grid
                              on the displacement lattice [-R, R]^2 (pixel
                              units) during dgdiff_solve_batch, for
                              dgdiff_mixture; 0 (default) = off */
+  int32_t windows;        /* N1 active windows ("the outer
+                             boundary is not reached"): 1 = sort this rank's
+                             sources spatially (Morton order) into source
+                             groups and, at every RK stage, compute only the
+                             rows / column strips inside each group's source
+                             box grown by one pixel per stage so far.  Exact:
+                             the 5-point operator spreads support by one pixel
+                             per stage, so everything outside is identically
+                             zero (results agree with windows = 0 to
+                             rounding; moments are returned in input order).
+                             Ring kernel only (kernel 1/2, temporal_steps 2 ->
+                             E_ARG).  0 (default) = whole grid */
 } dgdiff_opts;
 
 /* Fill *o with the defaults above. */

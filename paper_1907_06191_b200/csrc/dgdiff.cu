@@ -147,7 +147,9 @@ __global__ void __launch_bounds__(256) k_moments(const T *__restrict__ U, const 
 
 // sum the partials in CTA order; scale by h powers; write rows of the table
 __global__ void k_mom_reduce(const double *__restrict__ partial, int nblk, int64_t chunk, int64_t nvalid,
-                             double h, double *__restrict__ mom /* rows of this chunk */) {
+                             double h, double *__restrict__ mom /* rows of this chunk */,
+                             const int32_t *__restrict__ dest /* nullable: also scatter row s to */,
+                             double *__restrict__ mom_all /* row dest[s] (N1 sorted chunks) */) {
   int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= nvalid) return;
   double acc[6] = {0, 0, 0, 0, 0, 0};
@@ -164,6 +166,11 @@ __global__ void k_mom_reduce(const double *__restrict__ partial, int nblk, int64
   o[3] = acc[3] * h4;
   o[4] = acc[4] * h4;
   o[5] = acc[5] * h4;
+  if (dest) {
+    double *a = mom_all + (size_t)dest[s] * 6;
+#pragma unroll
+    for (int q = 0; q < 6; q++) a[q] = o[q];
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -221,13 +228,14 @@ __global__ void k_gather(const T *__restrict__ U, int nact, int g, int slot, dou
   out[r] = (double)U[((size_t)g * nact * D2 + r) * G + slot];
 }
 
-// source pixel -> active index for a chunk (padding slots repeat source 0)
+// source pixel -> active index for a chunk (padding slots repeat the last
+// valid source, so they never widen an N1 group box)
 __global__ void k_src_prep(const int32_t *__restrict__ src, int64_t nvalid, int64_t chunk,
                            const int *__restrict__ aidx, int nx, int *__restrict__ src_a,
                            int2 *__restrict__ src_ij) {
   int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= chunk) return;
-  int64_t k = s < nvalid ? s : 0;
+  int64_t k = s < nvalid ? s : nvalid - 1;
   int i = src[2 * k], j = src[2 * k + 1];
   src_a[s] = aidx[(size_t)j * nx + i];
   src_ij[s] = make_int2(i, j);
@@ -361,6 +369,18 @@ struct dgdiff_s {
   double *d_mom = nullptr;
   int64_t mom_cap = 0;
   double *d_out = nullptr;
+  // N1 active windows
+  bool windows = false;
+  int32_t *d_srcw = nullptr, *d_perm = nullptr;   // sorted local sources [nloc][2], their global indices
+  int64_t srcw_cap = 0;
+  double *d_momc = nullptr;                        // chunk-ordered moment rows (sorted order)
+  int64_t momc_cap = 0;
+  int4 *d_gbox = nullptr;                          // per group source box of the current chunk
+  int64_t gbox_cap = 0;
+  std::vector<int4> h_gbox;
+  std::vector<int64_t> h_spos;                     // local index -> sorted position
+  std::vector<int> h_pre;                          // 2-D prefix counts of active pixels [(ny+1)][(nx+1)]
+  int64_t last_chunk_pos0 = 0;                     // sorted position of the last chunk's first source
   // mixture grid (N2)
   double *d_mix = nullptr, *d_mix_out = nullptr;
   int mix_R = 0;
@@ -484,6 +504,10 @@ static void release(dgdiff_s *H) {
   cudaFree(H->d_out);
   cudaFree(H->d_mix);
   cudaFree(H->d_mix_out);
+  cudaFree(H->d_srcw);
+  cudaFree(H->d_perm);
+  cudaFree(H->d_momc);
+  cudaFree(H->d_gbox);
   if (H->comm && g_nccl.commDestroy) g_nccl.commDestroy(H->comm);
   if (H->own_stream && H->stream) cudaStreamDestroy(H->stream);
   delete H;
@@ -711,6 +735,16 @@ static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
     if (r != ncclSuccess) return fail(DGDIFF_E_NCCL, "ncclCommInitRank: %s", g_nccl.errStr(r));
   }
   H->st.n_active = H->nact;
+  H->windows = H->o.windows == 1;
+  if (H->windows) {
+    // 2-D prefix counts of extracellular pixels: algorithmic bytes of windowed stages
+    H->h_pre.assign((size_t)(ny + 1) * (nx + 1), 0);
+    for (int j = 0; j < ny; j++)
+      for (int i = 0; i < nx; i++)
+        H->h_pre[(size_t)(j + 1) * (nx + 1) + i + 1] = H->h_pre[(size_t)j * (nx + 1) + i + 1] +
+                                                       H->h_pre[(size_t)(j + 1) * (nx + 1) + i] -
+                                                       H->h_pre[(size_t)j * (nx + 1) + i] + (mask[(size_t)j * nx + i] ? 0 : 1);
+  }
   const char *sd = getenv("DGDIFF_STAGE_DETAIL");
   H->stage_detail = sd && sd[0] == '1';
   if (const char *ah = getenv("DGDIFF_AHEAD")) sscanf(ah, "%d,%d", &H->ahead_alpha, &H->ahead_noalpha);
@@ -733,6 +767,9 @@ extern "C" dgdiff_status dgdiff_create(dgdiff_t *out, const uint8_t *mask, int32
   if (o.outer_bc != 0 && o.outer_bc != 1) return fail(DGDIFF_E_ARG, "outer_bc must be 0 (REFLECT) or 1 (ABSORB)");
   if (o.outer_bc == 1 && (o.kernel == 1 || o.kernel == 2 || o.temporal_steps == 2))
     return fail(DGDIFF_E_ARG, "outer_bc ABSORB runs on the default ring kernel only");
+  if (o.windows != 0 && o.windows != 1) return fail(DGDIFF_E_ARG, "windows must be 0 or 1");
+  if (o.windows == 1 && (o.kernel == 1 || o.kernel == 2 || o.temporal_steps == 2))
+    return fail(DGDIFF_E_ARG, "windows (N1) run on the default ring kernel only");
   if (o.centering != 0 && o.centering != 1) return fail(DGDIFF_E_ARG, "centering must be 0 or 1");
   if (o.nranks < 1 || o.rank < 0 || o.rank >= o.nranks) return fail(DGDIFF_E_ARG, "bad rank/nranks");
   if (o.temporal_steps < 0) return fail(DGDIFF_E_ARG, "temporal_steps < 0");
@@ -780,6 +817,12 @@ static dgdiff_status run_chunk(dgdiff_s *H, int64_t nvalid, int64_t chunk, doubl
   int blocks = (int)std::min<int64_t>((nvec + 255) / 256, 148 * 64);
   k_init<T, NV, D2><<<blocks, 256, 0, st>>>(u, nvec, nact, H->d_src_a, iv);
   H->st.launches++;
+  if (H->windows) {
+    // N1: the stages write only inside the growing group boxes; the rest of
+    // the two work registers must read as zero
+    CK(cudaMemsetAsync(Ua, 0, sizeof(T) * (size_t)nvec * NV, st));
+    CK(cudaMemsetAsync(Ub, 0, sizeof(T) * (size_t)nvec * NV, st));
+  }
   // K2 x 3 per step (SSP-RK3 increment form, R7)
   const int wpb = std::min(ngroups, 4);
   const int px = 32;
@@ -832,12 +875,30 @@ static dgdiff_status run_chunk(dgdiff_s *H, int64_t nvalid, int64_t chunk, doubl
   sa.st = st;
   const int which = H->o.kernel == 1 ? 0 : H->o.kernel == 2 ? 1 : 2;
   const int prec = (int)(8 * sizeof(T));
+  // N1: extracellular pixels of group g's box grown by r (algorithmic bytes)
+  auto box_px = [&](int g, int r) -> double {
+    const int4 b = H->h_gbox[g];
+    const int x0 = std::max(0, b.x - r), x1 = std::min(H->nx - 1, b.y + r);
+    const int y0 = std::max(0, b.z - r), y1 = std::min(H->ny - 1, b.w + r);
+    const size_t W1 = (size_t)H->nx + 1;
+    return (double)(H->h_pre[(y1 + 1) * W1 + x1 + 1] - H->h_pre[(size_t)y0 * W1 + x1 + 1] -
+                    H->h_pre[(y1 + 1) * W1 + x0] + H->h_pre[(size_t)y0 * W1 + x0]);
+  };
+  double win_bytes = 0;
+  sa.gbox = H->windows ? H->d_gbox : nullptr;
+  int64_t cur_step = 0;
   auto stage = [&](int k, const T *Uin, T *Uout, double alpha, double cs) -> dgdiff_status {
     sa.Uin = Uin;
     sa.U0 = u;
     sa.Uout = Uout;
     sa.alpha = alpha;
     sa.cs = cs;
+    if (H->windows) {
+      sa.wr = (int)std::min<int64_t>(1 << 30, 3 * cur_step + k + 1);   // output support radius
+      double px = 0;
+      for (int g = 0; g < ngroups; g++) px += box_px(g, sa.wr);
+      win_bytes += (k == 0 ? 2.0 : 3.0) * px * D2 * G * sizeof(T);
+    }
     cudaError_t e = dgl::launch_stage(which, prec, P, k > 0, sa);
     if (e != cudaSuccess) return fail(DGDIFF_E_CUDA, "stage launch: %s", cudaGetErrorString(e));
     return DGDIFF_OK;
@@ -870,6 +931,7 @@ static dgdiff_status run_chunk(dgdiff_s *H, int64_t nvalid, int64_t chunk, doubl
   }
   for (int64_t s = 0; s < nsteps; s++) {
     const bool det = (s == 0);
+    cur_step = s;
     dgdiff_status r;
     if (det && (r = stage_ev(0, true)) != DGDIFF_OK) return r;
     if ((r = stage(0, u, Ua, 0.0, c)) != DGDIFF_OK) return r;
@@ -887,8 +949,8 @@ static dgdiff_status run_chunk(dgdiff_s *H, int64_t nvalid, int64_t chunk, doubl
   }
   H->st.launches += 3 * nsteps;
   H->st.stage_launches += 3 * nsteps;
-  H->st.stage_bytes += 8.0 * pass * nsteps;
-  H->st.stage_flops += fused_flops_per_step(H, chunk) * nsteps;
+  H->st.stage_bytes += H->windows ? win_bytes : 8.0 * pass * nsteps;
+  H->st.stage_flops += fused_flops_per_step(H, chunk) * nsteps * (H->windows ? win_bytes / std::max(1.0, 8.0 * pass * nsteps) : 1.0);
 after_stepping:
   CK(cudaGetLastError());
   // K4
@@ -904,7 +966,9 @@ after_stepping:
   dim3 mgrid(nblk, (ngroups + wpb - 1) / wpb);
   k_moments<T, NV, D2><<<mgrid, 32 * wpb, 0, st>>>(u, H->d_pix, H->d_src_ij, nact, ngroups, mpx, H->d_partial,
                                                chunk);
-  k_mom_reduce<<<(int)((nvalid + 127) / 128), 128, 0, st>>>(H->d_partial, nblk, chunk, nvalid, H->h, mom_rows);
+  k_mom_reduce<<<(int)((nvalid + 127) / 128), 128, 0, st>>>(H->d_partial, nblk, chunk, nvalid, H->h, mom_rows,
+                                                            H->windows ? H->d_perm + H->last_chunk_pos0 : nullptr,
+                                                            H->d_mom);
   H->st.launches += 2;
   if (H->mix_R > 0) {
     const int nc = (2 * H->mix_R + 1) * (2 * H->mix_R + 1);
@@ -981,6 +1045,40 @@ extern "C" dgdiff_status dgdiff_solve_batch(dgdiff_t H, const int32_t *sources, 
   }
   CK(cudaMemcpyAsync(H->d_src, sources, sizeof(int32_t) * 2 * n, cudaMemcpyHostToDevice, H->stream));
   H->st.h2d_bytes += sizeof(int32_t) * 2 * n;
+  std::vector<int32_t> srt;   // N1: this rank's sources in Morton order
+  if (nloc > 0 && H->windows) {
+    auto morton = [](uint32_t x, uint32_t y) {
+      uint64_t k = 0;
+      for (int bit = 0; bit < 16; bit++)
+        k |= (uint64_t)((x >> bit) & 1) << (2 * bit) | (uint64_t)((y >> bit) & 1) << (2 * bit + 1);
+      return k;
+    };
+    std::vector<int64_t> ord(nloc);
+    for (int64_t k = 0; k < nloc; k++) ord[k] = k;
+    std::stable_sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) {
+      return morton(sources[2 * (b + x)], sources[2 * (b + x) + 1]) <
+             morton(sources[2 * (b + y)], sources[2 * (b + y) + 1]);
+    });
+    srt.resize(2 * nloc);
+    std::vector<int32_t> perm(nloc);
+    H->h_spos.assign(nloc, 0);
+    for (int64_t k = 0; k < nloc; k++) {
+      srt[2 * k] = sources[2 * (b + ord[k])];
+      srt[2 * k + 1] = sources[2 * (b + ord[k]) + 1];
+      perm[k] = (int32_t)(b + ord[k]);
+      H->h_spos[ord[k]] = k;
+    }
+    if (nloc > H->srcw_cap) {
+      cudaFree(H->d_srcw); cudaFree(H->d_perm);
+      H->d_srcw = nullptr; H->d_perm = nullptr;
+      CK(cudaMalloc(&H->d_srcw, sizeof(int32_t) * 2 * nloc));
+      CK(cudaMalloc(&H->d_perm, sizeof(int32_t) * nloc));
+      H->srcw_cap = nloc;
+    }
+    CK(cudaMemcpyAsync(H->d_srcw, srt.data(), sizeof(int32_t) * 2 * nloc, cudaMemcpyHostToDevice, H->stream));
+    CK(cudaMemcpyAsync(H->d_perm, perm.data(), sizeof(int32_t) * nloc, cudaMemcpyHostToDevice, H->stream));
+    H->st.h2d_bytes += sizeof(int32_t) * 3 * nloc;
+  }
   if (nloc > 0) {
     // chunk size: fit 3 RK registers in free device memory
     const size_t per_src = 3 * (size_t)H->nact * H->D2 * tsize(H);
@@ -1017,10 +1115,40 @@ extern "C" dgdiff_status dgdiff_solve_batch(dgdiff_t H, const int32_t *sources, 
     for (int64_t c0 = 0; c0 < nloc; c0 += chunk) {
       int64_t nvalid = std::min(chunk, nloc - c0);
       int64_t cpad = (nvalid + G - 1) / G * G;
-      k_src_prep<<<(int)((cpad + 127) / 128), 128, 0, H->stream>>>(H->d_src + 2 * (b + c0), nvalid, cpad,
-                                                                 H->d_aidx, H->nx, H->d_src_a, H->d_src_ij);
+      const int32_t *srcp = H->windows ? H->d_srcw + 2 * c0 : H->d_src + 2 * (b + c0);
+      k_src_prep<<<(int)((cpad + 127) / 128), 128, 0, H->stream>>>(srcp, nvalid, cpad, H->d_aidx, H->nx,
+                                                                 H->d_src_a, H->d_src_ij);
       H->st.launches++;
       double *rows = H->d_mom + 6 * (b + c0);
+      if (H->windows) {
+        // per group: bounding box of its sources (padding repeats the last valid source)
+        const int64_t ng = cpad / G;
+        H->h_gbox.assign(ng, make_int4(INT32_MAX, INT32_MIN, INT32_MAX, INT32_MIN));
+        for (int64_t sl = 0; sl < cpad; sl++) {
+          const int64_t k = c0 + std::min(sl, nvalid - 1);
+          int4 &bx = H->h_gbox[sl / G];
+          bx.x = std::min(bx.x, srt[2 * k]);
+          bx.y = std::max(bx.y, srt[2 * k]);
+          bx.z = std::min(bx.z, srt[2 * k + 1]);
+          bx.w = std::max(bx.w, srt[2 * k + 1]);
+        }
+        if (ng > H->gbox_cap) {
+          cudaFree(H->d_gbox);
+          H->d_gbox = nullptr;
+          CK(cudaMalloc(&H->d_gbox, sizeof(int4) * ng));
+          H->gbox_cap = ng;
+        }
+        CK(cudaMemcpyAsync(H->d_gbox, H->h_gbox.data(), sizeof(int4) * ng, cudaMemcpyHostToDevice, H->stream));
+        H->st.h2d_bytes += sizeof(int4) * ng;
+        if (cpad > H->momc_cap) {
+          cudaFree(H->d_momc);
+          H->d_momc = nullptr;
+          CK(cudaMalloc(&H->d_momc, sizeof(double) * 6 * cpad));
+          H->momc_cap = cpad;
+        }
+        rows = H->d_momc;   // chunk order; k_mom_reduce scatters to the input order
+        H->last_chunk_pos0 = c0;
+      }
       dgdiff_status s = H->o.precision == 32 ? run_chunk_p<float>(H, nvalid, cpad, dt, nsteps, rows)
                                              : run_chunk_p<double>(H, nvalid, cpad, dt, nsteps, rows);
       if (s != DGDIFF_OK) return s;
@@ -1189,12 +1317,17 @@ extern "C" dgdiff_status dgdiff_source_moments(dgdiff_t H, double *out) {
 extern "C" dgdiff_status dgdiff_get_density(dgdiff_t H, int64_t src, double *out) {
   if (!H || !out) return fail(DGDIFF_E_ARG, "NULL argument");
   if (!H->solved || !H->o.keep_density) return fail(DGDIFF_E_STATE, "needs keep_density and a solve");
-  if (src < H->last_chunk_begin || src >= H->last_chunk_begin + H->last_chunk_n)
-    return fail(DGDIFF_E_STATE, "source %lld is not in this rank's last chunk [%lld, %lld)", (long long)src,
-                (long long)H->last_chunk_begin, (long long)(H->last_chunk_begin + H->last_chunk_n));
+  int64_t k = src - H->last_chunk_begin;
+  if (H->windows) {
+    // N1: chunks hold the rank's sources in Morton order
+    int64_t b, e;
+    dgdiff_shard(H->last_n, H->o.rank, H->o.nranks, &b, &e);
+    k = (src >= b && src < e) ? H->h_spos[src - b] - H->last_chunk_pos0 : -1;
+  }
+  if (k < 0 || k >= H->last_chunk_n)
+    return fail(DGDIFF_E_STATE, "source %lld is not in this rank's last chunk", (long long)src);
   CK(cudaSetDevice(H->dev));
   const int G = gsize(H);
-  int64_t k = src - H->last_chunk_begin;
   int g = (int)(k / G), slot = (int)(k % G);
   const int64_t nel = H->nact * H->D2;
   double *d_tmp = nullptr;

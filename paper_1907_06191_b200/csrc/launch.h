@@ -21,6 +21,11 @@ struct StageArgs {
   int ahead_alpha = 0, ahead_noalpha = 0;  // ring: max rows in flight (0 = default)
   int n1_use = 0, n2_use = 0;       // ring: slots used of rings 1 / 2 (0 = all)
   double alpha = 0, cs = 0;
+  // ring, N1 active windows: per source group the bounding box {x0, x1, y0, y1}
+  // of its sources; only output rows / strips within the box grown by wr
+  // pixels are computed (nullptr = the whole grid)
+  const int4 *gbox = nullptr;
+  int wr = 0;
   cudaStream_t st = nullptr;
 };
 

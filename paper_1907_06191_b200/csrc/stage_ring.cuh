@@ -96,6 +96,29 @@ struct RingGeom {
   static_assert(N1 >= 4 * (W + 2) && N2 >= 4 * W, "rings too small for progress");
 };
 
+// Work item -> (strip s, group g, computed rows [jb0, jb1)); false if the item
+// has nothing to compute.  With active windows (N1, gbox != nullptr) the rows
+// and strips are clipped to group g's source box grown by wr pixels: outside
+// it the stage's output is exactly zero (the 5-point operator spreads support
+// by one pixel per stage) and the registers already hold zeros there.
+template <int W>
+__device__ __forceinline__ bool ring_item(int item, int nstrips, int ngroups, int band_rows, int ny,
+                                          const int4 *__restrict__ gbox, int wr, int &s, int &g, int &jb0,
+                                          int &jb1) {
+  s = item % nstrips;
+  g = (item / nstrips) % ngroups;
+  const int b = item / (nstrips * ngroups);
+  jb0 = b * band_rows;
+  jb1 = min(ny, jb0 + band_rows);
+  if (gbox) {
+    const int4 bx = __ldg(&gbox[g]);
+    if (s * W > bx.y + wr || s * W + W - 1 < bx.x - wr) return false;
+    jb0 = max(jb0, bx.z - wr);
+    jb1 = min(jb1, bx.w + wr + 1);
+  }
+  return jb0 < jb1;
+}
+
 struct RowMeta {
   int p1, h0, c0, c1;   // ring-1 slot of tile start, active-index bounds
   int p2, pad0, pad1, pad2;
@@ -107,7 +130,7 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
     k_stage_ring(const T *__restrict__ Uin, const T *U0, T *Uout, const int4 *__restrict__ nbr,
                  const int4 *__restrict__ rowtab, int nact, int ny, int nstrips, int ngroups, int band_rows,
                  int nitems, T alpha, T cs, int diag, int max_ahead, int n1_use, int n2_use,
-                 const T *__restrict__ Aabs) {
+                 const T *__restrict__ Aabs, const int4 *__restrict__ gbox, int wr) {
   using Gm = RingGeom<T, NV, P, HAS_ALPHA>;
   constexpr int G = Gm::G, D2 = Gm::D2, PXB = Gm::PXB, Q = RING_Q, NC = Gm::NC;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -141,10 +164,8 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
     uint32_t v1 = 0, v2 = 0;        // virtual slot counters of rings 1 and 2
     uint32_t rel = 0;               // rows whose release has been observed
     for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-      const int s = item % nstrips;
-      const int g = (item / nstrips) % ngroups;
-      const int b = item / (nstrips * ngroups);
-      const int jb0 = b * band_rows, jb1 = min(ny, jb0 + band_rows);
+      int s, g, jb0, jb1;
+      if (!ring_item<Gm::W>(item, nstrips, ngroups, band_rows, ny, gbox, wr, s, g, jb0, jb1)) continue;
       const int lo = max(0, jb0 - 1), hi = min(ny - 1, jb1);
       __syncwarp();
       for (int r = lo + lane; r <= hi; r += 32) rt[r - lo] = __ldg(&rowtab[(size_t)s * ny + r]);
@@ -231,9 +252,8 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
   // cursor has passed row r + 1.
   uint32_t Lbase = 0;
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-    const int g = (item / nstrips) % ngroups;
-    const int b = item / (nstrips * ngroups);
-    const int jb0 = b * band_rows, jb1 = min(ny, jb0 + band_rows);
+    int s_, g, jb0, jb1;
+    if (!ring_item<Gm::W>(item, nstrips, ngroups, band_rows, ny, gbox, wr, s_, g, jb0, jb1)) continue;
     const int lo = max(0, jb0 - 1), hi = min(ny - 1, jb1);
     T *Uog = Uout + g * gstride + lane * NV;
     const T *U0l = U0 + g * gstride + lane * NV;
@@ -393,7 +413,7 @@ cudaError_t launch_ring(const dgl::StageArgs &a) {
       band_rows, nitems, (T)a.alpha, (T)a.cs, a.diag,
       std::max(4, std::min(RING_Q - 1, alpha_max_ahead(a, ALPHA))),
       Gm::R2U ? Gm::N1 : std::max(4 * (Gm::W + 2), std::min(Gm::N1, a.n1_use_na > 0 ? a.n1_use_na : Gm::N1)),
-      std::max(4 * Gm::W, std::min(Gm::N2, a.n2_use > 0 ? a.n2_use : Gm::N2)), (const T *)a.Aabs);
+      std::max(4 * Gm::W, std::min(Gm::N2, a.n2_use > 0 ? a.n2_use : Gm::N2)), (const T *)a.Aabs, a.gbox, a.wr);
   return cudaGetLastError();
 }
 

@@ -30,7 +30,7 @@ class dgdiff_opts(ctypes.Structure):
                 ("temporal_steps", ctypes.c_int32), ("device", ctypes.c_int32), ("rank", ctypes.c_int32),
                 ("nranks", ctypes.c_int32), ("nccl_id", ctypes.c_void_p), ("keep_density", ctypes.c_int32),
                 ("max_chunk", ctypes.c_int32), ("stream", ctypes.c_void_p), ("kernel", ctypes.c_int32),
-                ("mixture_radius", ctypes.c_int32)]
+                ("mixture_radius", ctypes.c_int32), ("windows", ctypes.c_int32)]
 
 
 class dgdiff_stats_t(ctypes.Structure):

@@ -494,3 +494,68 @@ def test_dg_vs_mc_gamma_substrate(dg, cfg, p, tol):
     for k in (0, 1):
         assert abs(S[k, k] - Sm[k, k]) <= tol * Sm[k, k] + 4 * se[2 * k]
         assert S[k, k] < 0.7 * 16.0 and Sm[k, k] < 0.7 * 16.0
+
+
+@pytest.mark.parametrize("p,prec,outer", [(1, 64, 0), (1, 32, 0), (2, 64, 0), (1, 64, 1)])
+def test_windows_bitwise_equal_whole_grid(dg, cfg, p, prec, outer):
+    """N1 active windows: Morton-sorted source groups, stages clipped to each
+    group's source box grown by one pixel per stage.  Every source's arithmetic
+    inside its support is unchanged and everything outside is exactly zero, so
+    moments and densities equal the whole-grid solve bit for bit -- across
+    several ragged chunks, sources near the grid edge (ABSORB boundary blocks)
+    and a box that outgrows the grid."""
+    m = cfg.mask("c3")
+    rng = np.random.default_rng(21)
+    free = np.argwhere(m == 0)
+    src = free[rng.choice(len(free), 300, replace=False)][:, ::-1].astype(np.int32)
+    edge = free[(free[:, 0] < 3) | (free[:, 1] > 508)][:4][:, ::-1].astype(np.int32)
+    src = np.concatenate([src, edge])
+    dt = 1 / 32 if p == 1 else 1 / 128
+    out = {}
+    for w in (0, 1):
+        with dg.Solver(m, 1.0, 1.0, p, precision=prec, keep_density=1, max_chunk=128, outer_bc=outer,
+                       mixture_radius=6, windows=w) as s:
+            s.solve(src, dt, 40)
+            S, mu = s.covariance()
+            n = len(src)
+            dens = {k: s.density(k) for k in range(n - 300, n, 37) if _in_last_chunk(s, k)}
+            out[w] = (s.moments(), S, mu, s.mixture(), dens, s.stats())
+    m0, m1 = out[0][0], out[1][0]
+    assert np.array_equal(m0, m1)
+    assert np.array_equal(out[0][1], out[1][1]) and np.array_equal(out[0][2], out[1][2])
+    g0, g1 = out[0][3][0], out[1][3][0]
+    assert np.abs(g0 - g1).max() <= 1e-13 * np.abs(g0).max()
+    common = set(out[0][4]) & set(out[1][4])
+    for k in common:
+        assert np.array_equal(out[0][4][k], out[1][4][k]), k
+    # the windowed solve moves fewer bytes
+    assert out[1][5]["stage_bytes"] < out[0][5]["stage_bytes"]
+
+
+def _in_last_chunk(s, k):
+    try:
+        s.density(k)
+        return True
+    except Exception:
+        return False
+
+
+def test_windows_c1_oracle(dg, orc, cfg):
+    """N1 windows on config c1 (one source next to the disk, 200 steps: the
+    box outgrows the 32^2 grid) against O1."""
+    m = cfg.mask("c1")
+    src = cfg.sources("c1")
+    c = cfg.CONFIGS["c1"]
+    ref_m, ref_d = orc.solve(1, 1.0, 1.0, m, src, c.dt, c.nsteps, keep_density=True)
+    for nst in (3, c.nsteps):
+        r_m, r_d = orc.solve(1, 1.0, 1.0, m, src, c.dt, nst, keep_density=True)
+        with dg.Solver(m, 1.0, 1.0, 1, keep_density=1, windows=1) as s:
+            s.solve(src, c.dt, nst)
+            got = s.density(0)
+            mom = s.moments()
+        assert rel_l2(got, r_d[0]) <= 1e-12
+        assert mom_err(mom, r_m) <= 1e-10
+        if nst == 3:   # after 3 steps = 9 stages the support is within 9 pixels (L1)
+            i0, j0 = src[0]
+            jj, ii = np.nonzero(np.abs(got).sum(axis=(2, 3)))
+            assert (np.abs(ii - i0) + np.abs(jj - j0)).max() <= 9

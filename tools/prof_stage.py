@@ -8,6 +8,7 @@ import argparse
 import json
 import os
 import sys
+import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -23,6 +24,7 @@ def main():
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--config", default="c4")
     ap.add_argument("--tb", type=int, default=0)
+    ap.add_argument("--windows", type=int, default=0)
     a = ap.parse_args()
     import torch
     torch.cuda.set_device(0)
@@ -32,17 +34,19 @@ def main():
     src = configs.sources(a.config)[:a.sources] if a.config != "c1" else configs.sources("c1")
     dt = 1 / 32 if a.degree == 1 else 1 / 128
     s = dg.Solver(m, 1.0, 1.0, a.degree, precision=a.precision, kernel=a.kernel, temporal_steps=a.tb,
-                  max_chunk=max(a.sources, 64))
+                  max_chunk=max(a.sources, 64), windows=a.windows)
     out = []
     for r in range(a.reps):
         dg.dgdiff_reset_stats(s.handle)
         dg.dgdiff_set_timing(s.handle, 1)
+        t0 = time.perf_counter()
         s.solve(src, dt, a.nsteps)
         S, mu = s.covariance()
+        wall = (time.perf_counter() - t0) * 1e3
         st = s.stats()
         ms = st["stage_ms"] / max(1, st["stage_launches"])
         gbs = st["stage_bytes"] / max(1, st["stage_launches"]) / (ms * 1e-3) / 1e9 if ms else 0
-        out.append(dict(rep=r, stage_ms=ms, gbs=gbs, launches=st["launches"], chunk=st["chunk"],
+        out.append(dict(rep=r, wall_ms=wall, stage_ms=ms, gbs=gbs, launches=st["launches"], chunk=st["chunk"],
                         sigma=[S[0, 0], S[0, 1], S[1, 1]]))
     print(json.dumps(dict(args=vars(a), runs=out)))
 
