@@ -64,6 +64,36 @@ struct InitVals { double v[2 * DMAXK]; };  // projected Dirac / h^2
 // ---------------------------------------------------------------------------
 // K1: zero the chunk's u and write the projected Dirac at each source pixel
 // ---------------------------------------------------------------------------
+// N1 windows: per group g only the active range [grange[g].x, grange[g].y)
+// (the rows the group's stages can read) is written, and the two work
+// registers Za, Zb are zeroed over the same range (blockIdx.y = group)
+template <typename T, int NV, int D2>
+__global__ void __launch_bounds__(256) k_init_win(T *__restrict__ U, T *__restrict__ Za, T *__restrict__ Zb,
+                                                  int nact, const int2 *__restrict__ grange,
+                                                  const int *__restrict__ src_a, InitVals iv) {
+  constexpr int G = 32 * NV;
+  const int g = blockIdx.y;
+  const int2 rg = __ldg(&grange[g]);
+  const int64_t base = ((int64_t)g * nact + rg.x) * D2 * 32;
+  const int64_t nvec = (int64_t)(rg.y - rg.x) * D2 * 32;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
+    const int lane = (int)(v & 31);
+    const int64_t r = v >> 5;
+    const int k = (int)(r % D2);
+    const int a = rg.x + (int)(r / D2);
+    T x[NV], z[NV];
+#pragma unroll
+    for (int e = 0; e < NV; e++) {
+      const int s = g * G + lane * NV + e;
+      x[e] = (__ldg(&src_a[s]) == a) ? (T)iv.v[k] : (T)0;
+      z[e] = (T)0;
+    }
+    stv<T, NV>(U + (base + v) * NV, x);
+    stv<T, NV>(Za + (base + v) * NV, z);
+    stv<T, NV>(Zb + (base + v) * NV, z);
+  }
+}
+
 template <typename T, int NV, int D2>
 __global__ void __launch_bounds__(256) k_init(T *__restrict__ U, int64_t nvec, int nact,
                                               const int *__restrict__ src_a, InitVals iv) {
@@ -97,7 +127,7 @@ template <typename T, int NV, int D2>
 __global__ void __launch_bounds__(256) k_moments(const T *__restrict__ U, const int2 *__restrict__ pix,
                                                  const int2 *__restrict__ src_ij, int nact, int ngroups,
                                                  int px_per_cta, double *__restrict__ partial,
-                                                 int64_t chunk) {
+                                                 int64_t chunk, const int2 *__restrict__ grange /* nullable (N1) */) {
   constexpr int G = 32 * NV, d = D2 / 2;
   const int lane = threadIdx.x & 31;
   const int g = blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -112,8 +142,13 @@ __global__ void __launch_bounds__(256) k_moments(const T *__restrict__ U, const 
 #pragma unroll
     for (int q = 0; q < 6; q++) m[q][e] = 0.0;
   }
-  const int a0 = blockIdx.x * px_per_cta;
-  const int a1 = min(nact, a0 + px_per_cta);
+  int a0 = blockIdx.x * px_per_cta;
+  int a1 = min(nact, a0 + px_per_cta);
+  if (grange) {   // N1: outside the group's range the state is zero (and not maintained)
+    const int2 rg = __ldg(&grange[g]);
+    a0 = max(a0, rg.x);
+    a1 = min(a1, rg.y);
+  }
   for (int a = a0; a < a1; a++) {
     const int2 ij = __ldg(&pix[a]);
     T c[D2][NV];
@@ -250,7 +285,7 @@ __global__ void k_src_prep(const int32_t *__restrict__ src, int64_t nvalid, int6
 template <typename T, int NV, int D2>
 __global__ void k_mixture(const T *__restrict__ U, const int *__restrict__ aidx, int nx, int ny, int nact,
                           const int2 *__restrict__ src_ij, const double *__restrict__ mom, int64_t nvalid, int R,
-                          double *__restrict__ grid) {
+                          double *__restrict__ grid, const int2 *__restrict__ grange /* nullable (N1) */) {
   constexpr int G = 32 * NV, d = D2 / 2;
   const int side = 2 * R + 1;
   const int cell = blockIdx.x * blockDim.x + threadIdx.x;
@@ -264,6 +299,10 @@ __global__ void k_mixture(const T *__restrict__ U, const int *__restrict__ aidx,
     const int a = __ldg(&aidx[(size_t)j * nx + i]);
     if (a < 0) continue;
     const int64_t g = s / G;
+    if (grange) {   // N1: outside the group's maintained range the density is exactly zero
+      const int2 rg = __ldg(&grange[g]);
+      if (a < rg.x || a >= rg.y) continue;
+    }
     const int slot = (int)(s % G);
     const T *p = U + ((size_t)g * nact + a) * D2 * G + slot;
     double vl = 0.0, vu = 0.0;
@@ -376,7 +415,9 @@ struct dgdiff_s {
   double *d_momc = nullptr;                        // chunk-ordered moment rows (sorted order)
   int64_t momc_cap = 0;
   int4 *d_gbox = nullptr;                          // per group source box of the current chunk
+  int2 *d_grange = nullptr;                        // per group maintained active range [a0, a1)
   int64_t gbox_cap = 0;
+  int wband = 32;                                  // ring band rows under windows (env DGDIFF_WBAND; swept 12-256 on c4)
   std::vector<int4> h_gbox;
   std::vector<int64_t> h_spos;                     // local index -> sorted position
   std::vector<int> h_pre;                          // 2-D prefix counts of active pixels [(ny+1)][(nx+1)]
@@ -508,6 +549,7 @@ static void release(dgdiff_s *H) {
   cudaFree(H->d_perm);
   cudaFree(H->d_momc);
   cudaFree(H->d_gbox);
+  cudaFree(H->d_grange);
   if (H->comm && g_nccl.commDestroy) g_nccl.commDestroy(H->comm);
   if (H->own_stream && H->stream) cudaStreamDestroy(H->stream);
   delete H;
@@ -749,6 +791,7 @@ static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
   H->stage_detail = sd && sd[0] == '1';
   if (const char *ah = getenv("DGDIFF_AHEAD")) sscanf(ah, "%d,%d", &H->ahead_alpha, &H->ahead_noalpha);
   if (const char *rg = getenv("DGDIFF_RING")) sscanf(rg, "%d,%d", &H->n1_use, &H->n2_use);
+  if (const char *wb = getenv("DGDIFF_WBAND")) H->wband = atoi(wb);
   return DGDIFF_OK;
 }
 
@@ -815,14 +858,16 @@ static dgdiff_status run_chunk(dgdiff_s *H, int64_t nvalid, int64_t chunk, doubl
   for (int k = 0; k < D2; k++) iv.v[k] = H->tab.init[k] * ih2;
   int64_t nvec = (int64_t)ngroups * nact * D2 * 32;
   int blocks = (int)std::min<int64_t>((nvec + 255) / 256, 148 * 64);
-  k_init<T, NV, D2><<<blocks, 256, 0, st>>>(u, nvec, nact, H->d_src_a, iv);
-  H->st.launches++;
   if (H->windows) {
-    // N1: the stages write only inside the growing group boxes; the rest of
-    // the two work registers must read as zero
-    CK(cudaMemsetAsync(Ua, 0, sizeof(T) * (size_t)nvec * NV, st));
-    CK(cudaMemsetAsync(Ub, 0, sizeof(T) * (size_t)nvec * NV, st));
+    // N1: the stages touch only the rows each group's growing box can reach;
+    // u and the two work registers are (re)initialised over exactly those rows
+    dim3 ig((unsigned)std::min<int64_t>(std::max<int64_t>(1, (nvec / std::max(1, ngroups) + 255) / 256), 2048),
+            (unsigned)ngroups);
+    k_init_win<T, NV, D2><<<ig, 256, 0, st>>>(u, Ua, Ub, nact, H->d_grange, H->d_src_a, iv);
+  } else {
+    k_init<T, NV, D2><<<blocks, 256, 0, st>>>(u, nvec, nact, H->d_src_a, iv);
   }
+  H->st.launches++;
   // K2 x 3 per step (SSP-RK3 increment form, R7)
   const int wpb = std::min(ngroups, 4);
   const int px = 32;
@@ -886,6 +931,7 @@ static dgdiff_status run_chunk(dgdiff_s *H, int64_t nvalid, int64_t chunk, doubl
   };
   double win_bytes = 0;
   sa.gbox = H->windows ? H->d_gbox : nullptr;
+  sa.band_rows = H->windows ? H->wband : 0;
   int64_t cur_step = 0;
   auto stage = [&](int k, const T *Uin, T *Uout, double alpha, double cs) -> dgdiff_status {
     sa.Uin = Uin;
@@ -965,7 +1011,7 @@ after_stepping:
   }
   dim3 mgrid(nblk, (ngroups + wpb - 1) / wpb);
   k_moments<T, NV, D2><<<mgrid, 32 * wpb, 0, st>>>(u, H->d_pix, H->d_src_ij, nact, ngroups, mpx, H->d_partial,
-                                               chunk);
+                                               chunk, H->windows ? H->d_grange : nullptr);
   k_mom_reduce<<<(int)((nvalid + 127) / 128), 128, 0, st>>>(H->d_partial, nblk, chunk, nvalid, H->h, mom_rows,
                                                             H->windows ? H->d_perm + H->last_chunk_pos0 : nullptr,
                                                             H->d_mom);
@@ -973,7 +1019,8 @@ after_stepping:
   if (H->mix_R > 0) {
     const int nc = (2 * H->mix_R + 1) * (2 * H->mix_R + 1);
     k_mixture<T, NV, D2><<<(nc + 127) / 128, 128, 0, st>>>(u, H->d_aidx, H->nx, H->ny, nact, H->d_src_ij, mom_rows,
-                                                         nvalid, H->mix_R, H->d_mix);
+                                                         nvalid, H->mix_R, H->d_mix,
+                                                         H->windows ? H->d_grange : nullptr);
     H->st.launches++;
   }
   CK(cudaGetLastError());
@@ -1132,14 +1179,27 @@ extern "C" dgdiff_status dgdiff_solve_batch(dgdiff_t H, const int32_t *sources, 
           bx.z = std::min(bx.z, srt[2 * k + 1]);
           bx.w = std::max(bx.w, srt[2 * k + 1]);
         }
+        // maintained active range per group: whole rows the group's stages can
+        // read, [y0 - R - 1, y1 + R + 1] with R = 3 nsteps (raster order: contiguous)
+        std::vector<int2> rng(ng);
+        const int64_t R = std::min<int64_t>(3 * nsteps + 1, H->ny);
+        for (int64_t g = 0; g < ng; g++) {
+          const int y0 = (int)std::max<int64_t>(0, H->h_gbox[g].z - R);
+          const int y1 = (int)std::min<int64_t>(H->ny, H->h_gbox[g].w + R + 1);
+          rng[g] = make_int2(H->h_pre[(size_t)y0 * (H->nx + 1) + H->nx], H->h_pre[(size_t)y1 * (H->nx + 1) + H->nx]);
+        }
         if (ng > H->gbox_cap) {
           cudaFree(H->d_gbox);
+          cudaFree(H->d_grange);
           H->d_gbox = nullptr;
+          H->d_grange = nullptr;
           CK(cudaMalloc(&H->d_gbox, sizeof(int4) * ng));
+          CK(cudaMalloc(&H->d_grange, sizeof(int2) * ng));
           H->gbox_cap = ng;
         }
         CK(cudaMemcpyAsync(H->d_gbox, H->h_gbox.data(), sizeof(int4) * ng, cudaMemcpyHostToDevice, H->stream));
-        H->st.h2d_bytes += sizeof(int4) * ng;
+        CK(cudaMemcpyAsync(H->d_grange, rng.data(), sizeof(int2) * ng, cudaMemcpyHostToDevice, H->stream));
+        H->st.h2d_bytes += (sizeof(int4) + sizeof(int2)) * ng;
         if (cpad > H->momc_cap) {
           cudaFree(H->d_momc);
           H->d_momc = nullptr;

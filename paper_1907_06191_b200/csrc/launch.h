@@ -26,6 +26,7 @@ struct StageArgs {
   // pixels are computed (nullptr = the whole grid)
   const int4 *gbox = nullptr;
   int wr = 0;
+  int band_rows = 0;                // ring: max rows per band (0 = heuristic)
   cudaStream_t st = nullptr;
 };
 

@@ -403,6 +403,7 @@ cudaError_t launch_ring(const dgl::StageArgs &a) {
   const int per_band = (ALPHA ? a.nstrips : a.nstrips_na) * a.ngroups;
   int nbands = std::max(1, std::min(a.ny, (8 * a.nsm + per_band - 1) / per_band));
   int band_rows = (a.ny + nbands - 1) / nbands;
+  if (a.band_rows > 0) band_rows = std::min(band_rows, a.band_rows);   // N1 windows: finer items
   if (band_rows > RING_MAXBAND) band_rows = RING_MAXBAND;
   nbands = (a.ny + band_rows - 1) / band_rows;
   const int nitems = per_band * nbands;
