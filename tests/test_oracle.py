@@ -260,6 +260,50 @@ def test_rotation_180_symmetry_exact(orc):
     assert np.allclose(mur, -mu, atol=1e-14)
 
 
+def _disks_mask(k, L=12.0):
+    """Fixed disk geometry on [0, L]^2 rasterised at h = 1/k (pixel centre in
+    a closed disk, reading R16)."""
+    n = int(L * k)
+    c = (np.arange(n) + 0.5) / k
+    X, Y = np.meshgrid(c, c)
+    m = np.zeros((n, n), np.uint8)
+    for cx, cy, r in [(3.1, 3.4, 1.6), (8.7, 4.2, 2.1), (4.6, 8.9, 1.9), (9.3, 9.6, 1.4)]:
+        m |= ((X - cx) ** 2 + (Y - cy) ** 2 <= r * r).astype(np.uint8)
+    return m
+
+
+def test_rotation_90_eigenvalues_converge(orc):
+    """90 degrees maps the LL->UR diagonals onto LR->UL ones, so the mesh is not
+    invariant and Sigma' = R Sigma R^T holds only to discretisation order
+    (north star: '90-degree-rotation invariance of Sigma's eigenvalues on
+    rotated substrates').  Free space: Sigma = 2 D Delta I + h^2[[1/20, 1/15],
+    [1/15, 1/20]] does not depend on where the source sits, so it is invariant
+    (to rounding).  Walled substrate at h = 1/2 and 1/4 (same disks, same
+    physical time): the eigenvalue mismatch shrinks with h (catches an
+    orientation-dependent flux or wall term that does not vanish)."""
+    def eig(mask, src, k, nsteps):
+        n = mask.shape[0]
+        S, _ = orc.sigma(orc.solve(1, 1.0 / k, 1.0, mask, src, 1 / 32 / k ** 2, nsteps))
+        Sr, _ = orc.sigma(orc.solve(1, 1.0 / k, 1.0, np.rot90(mask).copy(),
+                                    [(j, n - 1 - i) for i, j in src], 1 / 32 / k ** 2, nsteps))
+        return np.linalg.eigvalsh(S), np.linalg.eigvalsh(Sr)
+    # free space (walls >= 15 sigma away): Sigma itself is unchanged
+    free = np.zeros((64, 64), np.uint8)
+    e, er = eig(free, [(32, 32), (30, 33)], 1, 48)
+    assert np.allclose(e, er, rtol=1e-12, atol=0)
+    # walled: convergence in h
+    diffs = []
+    for k in (2, 4):
+        m = _disks_mask(k)
+        pts = [(6.1, 6.3), (5.9, 2.2), (2.6, 6.4)]          # physical source points (extracellular)
+        src = [(int(x * k), int(y * k)) for x, y in pts]
+        assert all(m[j, i] == 0 for i, j in src)
+        e, er = eig(m, src, k, 32 * k * k)                   # physical time 1.0
+        diffs.append(np.abs(e - er).max() / e.max())
+    assert diffs[1] < 0.75 * diffs[0], diffs
+    assert diffs[1] < 0.02, diffs
+
+
 def test_sigma_symmetric_psd_and_hindered(orc):
     """Sigma stored symmetric; eigenvalues > 0; walls hinder: Sigma_ii < 2 D Delta
     (the paper's case study 19.50 < 32.4)."""
