@@ -55,7 +55,7 @@ static dgdiff_status fail(dgdiff_status s, const char *fmt, ...) {
 // ---------------------------------------------------------------------------
 // device constants
 // ---------------------------------------------------------------------------
-#define DMAXK 6                    // max dofs per triangle on the GPU path (P2)
+#define DMAXK 10                   // max dofs per triangle on the GPU path (P3)
 __constant__ double c_W[2 * 6 * DMAXK];    // moment weights (unit pixel)
 __constant__ double c_CW[2 * DMAXK];       // basis values at the pixel centre (mixture nodes)
 
@@ -492,8 +492,9 @@ extern "C" const char *dgdiff_last_error(void) { return g_err.c_str(); }
 
 extern "C" double dgdiff_dt_max(int32_t degree, double h, double D) {
   // SSP-RK3 real-axis stability limit 2.5127453 over the Bloch spectral radius
-  // of the composite operator (R8): rho_1 = 60, rho_2 = 192.7953
-  double rho = degree == 1 ? 60.0 : degree == 2 ? 192.7953 : 0.0;
+  // of the composite operator (R8): rho_1 = 60, rho_2 = 192.7953,
+  // rho_3 = 462.37
+  double rho = degree == 1 ? 60.0 : degree == 2 ? 192.7953 : degree == 3 ? 462.37 : 0.0;
   if (rho == 0.0 || !(h > 0) || !(D > 0)) return 0.0;
   return 2.5127453 / rho * h * h / D;
 }
@@ -507,7 +508,7 @@ extern "C" void dgdiff_shard(int64_t n, int32_t rank, int32_t nranks, int64_t *b
 }
 
 extern "C" dgdiff_status dgdiff_operator_table(int32_t degree, double *A, double *W, double *init) {
-  if (degree < 1 || degree > 2) return fail(DGDIFF_E_ARG, "degree %d not supported (1 or 2)", degree);
+  if (degree < 1 || degree > 3) return fail(DGDIFF_E_ARG, "degree %d not supported (1..3)", degree);
   try {
     dgop::Table T = dgop::build(degree);
     if (A) memcpy(A, T.A.data(), T.A.size() * sizeof(double));
@@ -601,11 +602,15 @@ static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
     for (int code = 0; code < 16; code++)
       for (int r = 0; r < D2; r++)
         for (int c = 0; c < D2; c++) {
-          auto tb = [&](int b) { return H->p == 1 ? dgk::tab<1>(b, r, c) : dgk::tab<2>(b, r, c); };
-          double self = tb(0);
+          auto tb = [&](int b) {
+            return H->p == 1 ? dgk::tab<1>(b, r, c) : H->p == 2 ? dgk::tab<2>(b, r, c) : dgk::tab<3>(b, r, c);
+          };
+          if (tb(9 + code) != A(code, 0, r, c)) return fail(DGDIFF_E_ARG, "compiled operator table differs from K0 (self)");
+          double self = tb(0);   // V + sum of the open F_f: exact on the dyadic P1/P2 tables
           for (int f = 0; f < 4; f++)
             if ((code >> f) & 1) self += tb(1 + f);
-          if (self != A(code, 0, r, c)) return fail(DGDIFF_E_ARG, "compiled operator table differs from K0 (self)");
+          if (H->p <= 2 && self != A(code, 0, r, c))
+            return fail(DGDIFF_E_ARG, "compiled operator table differs from K0 (V + F)");
           for (int f = 0; f < 4; f++)
             if (A(code, 1 + f, r, c) != (((code >> f) & 1) ? tb(5 + f) : 0.0))
               return fail(DGDIFF_E_ARG, "compiled operator table differs from K0 (neighbour)");
@@ -803,7 +808,7 @@ extern "C" dgdiff_status dgdiff_create(dgdiff_t *out, const uint8_t *mask, int32
   if ((int64_t)nx * ny >= (1LL << 31)) return fail(DGDIFF_E_ARG, "grid too large");
   if (!(h > 0) || !(D > 0) || !std::isfinite(h) || !std::isfinite(D))
     return fail(DGDIFF_E_ARG, "h and D must be positive and finite");
-  if (degree < 1 || degree > 2) return fail(DGDIFF_E_ARG, "degree %d not supported (1 or 2)", degree);
+  if (degree < 1 || degree > 3) return fail(DGDIFF_E_ARG, "degree %d not supported (1..3)", degree);
   dgdiff_opts o;
   if (opts) o = *opts; else dgdiff_opts_default(&o);
   if (o.precision != 32 && o.precision != 64) return fail(DGDIFF_E_ARG, "precision must be 32 or 64");
@@ -811,6 +816,8 @@ extern "C" dgdiff_status dgdiff_create(dgdiff_t *out, const uint8_t *mask, int32
   if (o.outer_bc == 1 && (o.kernel == 1 || o.kernel == 2 || o.temporal_steps == 2))
     return fail(DGDIFF_E_ARG, "outer_bc ABSORB runs on the default ring kernel only");
   if (o.windows != 0 && o.windows != 1) return fail(DGDIFF_E_ARG, "windows must be 0 or 1");
+  if (degree == 3 && (o.kernel == 1 || o.kernel == 2 || o.temporal_steps == 2 || o.outer_bc != 0))
+    return fail(DGDIFF_E_ARG, "P3 (N4) runs on the default ring kernel with REFLECT only");
   if (o.windows == 1 && (o.kernel == 1 || o.kernel == 2 || o.temporal_steps == 2))
     return fail(DGDIFF_E_ARG, "windows (N1) run on the default ring kernel only");
   if (o.centering != 0 && o.centering != 1) return fail(DGDIFF_E_ARG, "centering must be 0 or 1");
@@ -896,7 +903,7 @@ static dgdiff_status run_chunk(dgdiff_s *H, int64_t nvalid, int64_t chunk, doubl
     if (!begin) H->sev_pending[k] = true;
     return DGDIFF_OK;
   };
-  constexpr int P = D2 == 6 ? 1 : 2;
+  constexpr int P = D2 == 6 ? 1 : D2 == 12 ? 2 : 3;
   dgl::StageArgs sa;
   sa.nbr = H->d_nbr;
   sa.A = A;
@@ -1033,10 +1040,12 @@ static dgdiff_status run_chunk_p(dgdiff_s *H, int64_t nvalid, int64_t chunk, dou
   const int nv = lane_nv(H);
   if (nv == 1) {
     if (H->D2 == 6) return run_chunk<T, 1, 6>(H, nvalid, chunk, dt, nsteps, mom_rows);
+    if (H->D2 == 20) return run_chunk<T, 1, 20>(H, nvalid, chunk, dt, nsteps, mom_rows);
     return run_chunk<T, 1, 12>(H, nvalid, chunk, dt, nsteps, mom_rows);
   }
   if (nv == 2) {
     if (H->D2 == 6) return run_chunk<T, 2, 6>(H, nvalid, chunk, dt, nsteps, mom_rows);
+    if (H->D2 == 20) return run_chunk<T, 2, 20>(H, nvalid, chunk, dt, nsteps, mom_rows);
     return run_chunk<T, 2, 12>(H, nvalid, chunk, dt, nsteps, mom_rows);
   }
   if constexpr (sizeof(T) == 4) {
@@ -1354,7 +1363,7 @@ extern "C" dgdiff_status dgdiff_absorb_table(int32_t degree, double *A) {
 }
 
 extern "C" dgdiff_status dgdiff_centre_weights(int32_t degree, double *cw) {
-  if (degree < 1 || degree > 2) return fail(DGDIFF_E_ARG, "degree %d not supported (1 or 2)", degree);
+  if (degree < 1 || degree > 3) return fail(DGDIFF_E_ARG, "degree %d not supported (1..3)", degree);
   if (!cw) return fail(DGDIFF_E_ARG, "cw is NULL");
   try {
     dgop::Table T = dgop::build(degree);
@@ -1396,6 +1405,7 @@ extern "C" dgdiff_status dgdiff_get_density(dgdiff_t H, int64_t src, double *out
   const int nv = lane_nv(H);
 #define DG_GATHER(TT, NVV)                                                                                     \
   if (H->D2 == 6) k_gather<TT, NVV, 6><<<blocks, 256, 0, H->stream>>>((TT *)H->d_U[0], (int)H->nact, g, slot, d_tmp); \
+  else if (H->D2 == 20) k_gather<TT, NVV, 20><<<blocks, 256, 0, H->stream>>>((TT *)H->d_U[0], (int)H->nact, g, slot, d_tmp); \
   else k_gather<TT, NVV, 12><<<blocks, 256, 0, H->stream>>>((TT *)H->d_U[0], (int)H->nact, g, slot, d_tmp);
   if (H->o.precision == 32) {
     if (nv == 1) { DG_GATHER(float, 1) } else if (nv == 2) { DG_GATHER(float, 2) } else { DG_GATHER(float, 4) }

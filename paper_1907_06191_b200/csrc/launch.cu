@@ -12,6 +12,11 @@ int ring_width(int P, bool alpha) {
     return m == RING_PLAIN ? RingCfg<1, 16, RING_PLAIN>::W
            : m == RING_U0_STAGED ? RingCfg<1, 16, RING_U0_STAGED>::W : RingCfg<1, 16, RING_U0_DIRECT>::W;
   }
+  if (P == 3) {
+    const int m = ring_mode<3>(alpha);
+    return m == RING_PLAIN ? RingCfg<3, 8, RING_PLAIN>::W
+           : m == RING_U0_STAGED ? RingCfg<3, 8, RING_U0_STAGED>::W : RingCfg<3, 8, RING_U0_DIRECT>::W;
+  }
   const int m = ring_mode<2>(alpha);
   return m == RING_PLAIN ? RingCfg<2, 8, RING_PLAIN>::W
          : m == RING_U0_STAGED ? RingCfg<2, 8, RING_U0_STAGED>::W : RingCfg<2, 8, RING_U0_DIRECT>::W;
@@ -21,6 +26,7 @@ cudaError_t launch_stage(int which, int prec, int P, bool alpha, const StageArgs
   if (which == 0 || which == 1)
     return prec == 64 ? launch_v12_f64(which, P, alpha, a) : launch_v12_f32(which, P, alpha, a);
   if (P == 1) return prec == 64 ? launch_ring_p1_f64(alpha, a) : launch_ring_p1_f32(alpha, a);
+  if (P == 3) return prec == 64 ? launch_ring_p3_f64(alpha, a) : launch_ring_p3_f32(alpha, a);
   return prec == 64 ? launch_ring_p2_f64(alpha, a) : launch_ring_p2_f32(alpha, a);
 }
 

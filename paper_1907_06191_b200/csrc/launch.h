@@ -47,5 +47,7 @@ cudaError_t launch_ring_p1_f64(bool alpha, const StageArgs &a);
 cudaError_t launch_ring_p1_f32(bool alpha, const StageArgs &a);
 cudaError_t launch_ring_p2_f64(bool alpha, const StageArgs &a);
 cudaError_t launch_ring_p2_f32(bool alpha, const StageArgs &a);
+cudaError_t launch_ring_p3_f64(bool alpha, const StageArgs &a);
+cudaError_t launch_ring_p3_f32(bool alpha, const StageArgs &a);
 
 }  // namespace dgl

@@ -351,7 +351,9 @@ Table build(int p) {
                 continue;
               }
               if (!used) continue;
-              if (!dyadic(q)) throw std::runtime_error("composite entry is not dyadic");
+              // P1/P2 entries are dyadic (exact in fp32 and fp64); P3 entries are
+              // not and are rounded to the nearest double (fp32: float)
+              if (p <= 2 && !dyadic(q)) throw std::runtime_error("composite entry is not dyadic");
               T.A[(((size_t)code * 5 + o) * D2 + r) * D2 + t * d + j] = q.to_double();
               if (!q.zero()) T.nnz[code * 5 + o]++;
             }

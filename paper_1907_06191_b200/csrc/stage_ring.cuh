@@ -67,6 +67,10 @@ template <> struct RingCfg<1, 16, RING_U0_DIRECT> { static constexpr int W = 16,
 template <> struct RingCfg<2, 8, RING_PLAIN> { static constexpr int W = 16, NC = 16; };   // c5: W 8 -> 16 -29 %
 template <> struct RingCfg<2, 8, RING_U0_STAGED> { static constexpr int W = 8, NC = 16; };
 template <> struct RingCfg<2, 8, RING_U0_DIRECT> { static constexpr int W = 16, NC = 12; };   // c5: NC 8 -> 12 -4 %
+// P3 (N4): 5 KB pixel tiles (fp64), four halo'd rows of W = 8 fill ring 1
+template <> struct RingCfg<3, 8, RING_PLAIN> { static constexpr int W = 8, NC = 8; };
+template <> struct RingCfg<3, 8, RING_U0_STAGED> { static constexpr int W = 8, NC = 8; };
+template <> struct RingCfg<3, 8, RING_U0_DIRECT> { static constexpr int W = 8, NC = 8; };
 template <int P> constexpr int ring_mode(bool alpha) {
   return alpha ? (ring_u0_direct<P>() ? RING_U0_DIRECT : RING_U0_STAGED) : RING_PLAIN;
 }
@@ -315,20 +319,26 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
       if (__builtin_expect(outer == 0, 1)) {
         // self block of this pixel's open-face code (compile-time immediates),
         // then the fixed neighbour blocks of the open faces
-        mv_self<T, NV, P>(open_code(nb), acc, xs);
+        // (P3: 400-entry blocks; a 16-variant switch would not fit the
+        // instruction cache, so the self block is applied as V + sum F_f)
+        if constexpr (P <= 2) mv_self<T, NV, P>(open_code(nb), acc, xs);
+        else mv_imm<T, NV, P, 0>(acc, xs);
         if (nb.x >= 0) {
+          if constexpr (P == 3) mv_imm<T, NV, P, 1>(acc, xs);
           const T *pn = tile1(mc, nb.x);
 #pragma unroll
           for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
           mv_imm<T, NV, P, 5>(acc, xn);
         }
         if (nb.y >= 0) {
+          if constexpr (P == 3) mv_imm<T, NV, P, 2>(acc, xs);
           const T *pn = tile1(mc, nb.y);
 #pragma unroll
           for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
           mv_imm<T, NV, P, 6>(acc, xn);
         }
         if (nb.z >= 0) {
+          if constexpr (P == 3) mv_imm<T, NV, P, 3>(acc, xs);
           const RowMeta mn = meta[seq(j + 1) % Q];
           const T *pn = tile1(mn, nb.z);
 #pragma unroll
@@ -336,13 +346,14 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
           mv_imm<T, NV, P, 7>(acc, xn);
         }
         if (nb.w >= 0) {
+          if constexpr (P == 3) mv_imm<T, NV, P, 4>(acc, xs);
           const RowMeta ms = meta[seq(j - 1) % Q];
           const T *pn = tile1(ms, nb.w);
 #pragma unroll
           for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
           mv_imm<T, NV, P, 8>(acc, xn);
         }
-      } else {
+      } else if constexpr (P <= 2) {
         // boundary pixel with absorbing outer faces: blocks of (code, outer)
         // read from the K0 table in global memory (rare: grid-edge pixels)
         const T *Ab = Aabs + (size_t)((open_code(nb) * 16 + outer) * 5) * D2 * D2;

@@ -42,7 +42,7 @@ def test_library_is_sm100a(dg):
     assert "sm_100a" in out
 
 
-@pytest.mark.parametrize("p", [1, 2])
+@pytest.mark.parametrize("p", [1, 2, 3])
 def test_operator_table_matches_dense_assembly(dg, p):
     """K0 (exact rationals, monomial Vandermonde, q eliminated on a 3x3 patch)
     == blocks of O2's dense operator, for all 16 open-face codes."""
@@ -55,9 +55,11 @@ def test_operator_table_matches_dense_assembly(dg, p):
         for o, off in enumerate(offs):
             used = o == 0 or (code >> (o - 1)) & 1
             ref = blocks[off] if used else np.zeros_like(blocks[off])
-            assert np.allclose(A[code, o], ref, atol=1e-11), (code, o)
-    assert np.allclose(W, O2.moment_weights(p), atol=1e-15)
-    assert np.allclose(init, O2.delta(p, 1.0, 1, 1, (0, 0))[0, 0], atol=1e-13)
+            # (O2's floating-point Vandermonde inverse loses ~1e-12 relative at P3)
+            assert np.allclose(A[code, o], ref, atol=1e-11 * max(1.0, np.abs(ref).max())), (code, o)
+    tol = 1e-15 if p <= 2 else 1e-12     # O2's P3 Vandermonde inverse: ~1e-13 rounding
+    assert np.allclose(W, O2.moment_weights(p), atol=tol)
+    assert np.allclose(init, O2.delta(p, 1.0, 1, 1, (0, 0))[0, 0], atol=1e-13 if p <= 2 else 1e-10)
 
 
 def test_p1_table_is_survey_A11(dg):
@@ -112,7 +114,7 @@ def composite_apply(A, mask, u):
     return out
 
 
-@pytest.mark.parametrize("p", [1, 2])
+@pytest.mark.parametrize("p", [1, 2, 3])
 def test_table_reproduces_oracle_operator(dg, p, orc):
     """On random masks (all 16 codes, outer walls), the K0 table applied pixel
     by pixel equals O1's element-loop L(u) scaled by h^2/D, and conserves
@@ -180,7 +182,12 @@ def test_absorb_table_reproduces_oracle_operator(dg, p, orc):
 def test_dt_max_and_shard(dg):
     assert abs(dg.dgdiff_dt_max(1, 1.0, 1.0) - 2.5127453 / 60) < 1e-15
     assert abs(dg.dgdiff_dt_max(1, 0.5, 2.0) - 2.5127453 / 60 * 0.125) < 1e-15
-    assert dg.dgdiff_dt_max(3, 1.0, 1.0) == 0.0
+    assert abs(dg.dgdiff_dt_max(3, 1.0, 1.0) - 2.5127453 / 462.37) < 1e-15
+    assert dg.dgdiff_dt_max(4, 1.0, 1.0) == 0.0
+    # the P3 limit sits inside the stability interval of the assembled operator
+    from oracle import dense as O2
+    lam = np.linalg.eigvals(O2.assemble(3, 1.0, 1.0, np.zeros((8, 8), np.uint8)))
+    assert np.abs(lam).max() * dg.dgdiff_dt_max(3, 1.0, 1.0) < 2.5127453
     n = 65537
     spans = [dg.dgdiff_shard(n, r, 8) for r in range(8)]
     assert spans[0][0] == 0 and spans[-1][1] == n
@@ -200,8 +207,13 @@ def test_no_cpu_fallback(dg):
 
 def test_argument_errors_are_reported(dg):
     with pytest.raises(dg.DGDiffError) as e:
-        dg.dgdiff_create(np.zeros((4, 4), np.uint8), 1.0, 1.0, 3)
+        dg.dgdiff_create(np.zeros((4, 4), np.uint8), 1.0, 1.0, 4)
     assert e.value.status == dg.E_ARG
+    # P3 (N4): ring kernel and REFLECT only
+    for bad in (dict(kernel=1), dict(outer_bc=1), dict(temporal_steps=2)):
+        with pytest.raises(dg.DGDiffError) as e:
+            dg.dgdiff_create(np.zeros((4, 4), np.uint8), 1.0, 1.0, 3, dg.dgdiff_opts_default(**bad))
+        assert e.value.status == dg.E_ARG, bad
     with pytest.raises(dg.DGDiffError) as e:
         dg.dgdiff_create(np.zeros((4, 4), np.uint8), -1.0, 1.0, 1)
     assert e.value.status == dg.E_ARG

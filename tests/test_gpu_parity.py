@@ -559,3 +559,37 @@ def test_windows_c1_oracle(dg, orc, cfg):
             i0, j0 = src[0]
             jj, ii = np.nonzero(np.abs(got).sum(axis=(2, 3)))
             assert (np.abs(ii - i0) + np.abs(jj - j0)).max() <= 9
+
+
+@pytest.mark.parametrize("prec", [64, 32])
+def test_p3_random_masks_and_free_space(dg, orc, prec):
+    """N4: P3 on the ring kernel (V + sum F_f self blocks, non-dyadic
+    coefficients rounded to the state precision) against O1 on a random mask
+    with a ragged two-chunk batch, and the free-space closed form
+    Sigma = 2 D Delta I (P3 reproduces quadratics)."""
+    rng = np.random.default_rng(300 + prec)
+    ny, nx = 21, 27
+    m = (rng.random((ny, nx)) < 0.4).astype(np.uint8)
+    free = np.argwhere(m == 0)
+    G = 32 if prec == 64 else 64
+    n = G + 7
+    pick = free[rng.integers(0, len(free), n)]
+    src = np.stack([pick[:, 1], pick[:, 0]], 1).astype(np.int32)
+    dt = 1 / 256 * 0.64 / 1.7
+    ref_m, ref_d = orc.solve(3, 0.8, 1.7, m, src, dt, 50, keep_density=True)
+    with dg.Solver(m, 0.8, 1.7, 3, precision=prec, keep_density=1, max_chunk=G) as s:
+        s.solve(src, dt, 50)
+        S, mu = s.covariance()
+        mom = s.moments()
+        dens = [s.density(k) for k in range(G, n)]
+    t = TOL[prec]
+    for k, dk in zip(range(G, n), dens):
+        assert rel_l2(dk, ref_d[k]) <= t["dens"], k
+    assert mom_err(mom, ref_m) <= t["mom"]
+    R, _ = orc.sigma(ref_m)
+    assert sig_err(S, R) <= t["sig"]
+    fm = np.zeros((96, 96), np.uint8)
+    with dg.Solver(fm, 1.0, 1.0, 3, precision=prec) as s:
+        s.solve(np.array([[48, 48], [47, 49], [49, 47]], np.int32), 1 / 256, 256)
+        S, mu = s.covariance()
+    assert np.abs(S - 2.0 * np.eye(2)).max() <= (1e-11 if prec == 64 else 2e-4)

@@ -210,6 +210,16 @@ def test_free_space_sigma_p2_closed_form(orc):
     assert np.allclose(S, 2 * D * nsteps * dt * np.eye(2), rtol=0, atol=2e-12)
 
 
+def test_free_space_sigma_p3_closed_form(orc):
+    """P3 reproduces quadratics, so like P2 the projected Dirac has Sigma(0) = 0
+    and free-space Sigma = 2 D Delta I (walls 32 sigma away: 5e-13).  Catches
+    a P3 basis / quadrature / face-node error that P1/P2 pins cannot see."""
+    m = np.zeros((64, 64), np.uint8)
+    S, mu = orc.sigma(orc.solve(3, 1.0, 1.0, m, [(32, 32)], 1 / 256, 128))
+    assert np.abs(S - 1.0 * np.eye(2)).max() <= 2e-12
+    assert np.abs(mu).max() <= 1e-13
+
+
 def test_paper_analytic_value(orc):
     """k = 450 um^2/s, T = 0.036 s gives 2Tk = 32.4.  The same
     physics in grid units (h = 0.125 um) on a smaller free grid: P2 gives

@@ -32,7 +32,7 @@ def main():
     from paper_1907_06191_b200 import dgdiff as dg
     m = configs.mask(a.config)
     src = configs.sources(a.config)[:a.sources] if a.config != "c1" else configs.sources("c1")
-    dt = 1 / 32 if a.degree == 1 else 1 / 128
+    dt = {1: 1 / 32, 2: 1 / 128, 3: 1 / 256}[a.degree]
     s = dg.Solver(m, 1.0, 1.0, a.degree, precision=a.precision, kernel=a.kernel, temporal_steps=a.tb,
                   max_chunk=max(a.sources, 64), windows=a.windows)
     out = []
