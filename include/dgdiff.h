@@ -105,7 +105,8 @@ void dgdiff_opts_default(dgdiff_opts *o);
  *         (k = D); copied.
  *  h, D   pixel side and extracellular diffusivity k0 (> 0).
  *  degree Lagrange degree p of the triangle elements (Eq. (8); "p <= 3
- *         suffices"): 1 or 2 (3 -> E_ARG in this version).
+ *         suffices"): 1, 2 or 3 (P3: default ring kernel, REFLECT only; its
+ *         non-dyadic operator entries are rounded once to the state type).
  * Builds the operator tables (host), the open-face code of every pixel and the
  * active-pixel index, copies them to the device; when nranks > 1 initialises
  * NCCL from opts->nccl_id.  On failure *out is NULL. */
@@ -122,6 +123,21 @@ dgdiff_status dgdiff_create(dgdiff_t *out, const uint8_t *mask, int32_t nx, int3
  * this rank's shard are in the device moment table. */
 dgdiff_status dgdiff_solve_batch(dgdiff_t, const int32_t *sources, int64_t n, double dt,
                                  int64_t nsteps);
+
+/* N4: as dgdiff_solve_batch, for point sources anywhere in the extracellular
+ * pixels ("m points chosen uniformly in Omega_e").
+ *  points [n][2] (x, y) in physical units, 0 <= x < nx*h, 0 <= y < ny*h;
+ *         copied.  The point belongs to pixel (floor(x/h), floor(y/h)) (a
+ *         point on a pixel edge goes to the pixel above / right of it:
+ *         DESIGN.md reading R21); its Dirac is L2-projected onto the triangle
+ *         containing it (L: eta < xi, U: eta > xi; on the diagonal split 1/2 -
+ *         1/2 as for pixel centres, R10), and its moments are taken about the
+ *         point itself (R12).  A point at a pixel centre reproduces
+ *         dgdiff_solve_batch exactly.  E_SOURCE: non-finite, outside the grid
+ *         or in an axon pixel.  The mixture lattice (dgdiff_mixture) is not
+ *         accumulated for point sources (-> E_STATE there). */
+dgdiff_status dgdiff_solve_batch_points(dgdiff_t, const double *points, int64_t n, double dt,
+                                        int64_t nsteps);
 
 /* Steps 2-4 of P:243-265: centre + normalise each density, mix, and return
  * the mixture's covariance.  delta must equal nsteps*dt of the last solve

@@ -430,23 +430,32 @@ static void apply_L(const prob_t *P, const double *u, double *q, double *Lu) {
     }
 }
 
-/* Dirac Cauchy data at the centre of pixel (is,js): exact L2
- * projection, M_T u_T = N_T(x_c), split 1/2, 1/2 between L and U (R10).    */
-static void project_delta(const prob_t *P, int is, int js, double *u) {
+/* Dirac Cauchy data at the pixel-local point (xi, eta) of pixel (is,js)
+ * (P:241): exact L2 projection M_T u_T = N_T(x_s) on the triangle holding
+ * the point (L: eta < xi, U: eta > xi); a point on the shared diagonal (the
+ * pixel centre, R10) is split 1/2, 1/2 between L and U.  Sub-pixel points
+ * (N4) follow reading R21 (a point on a pixel edge belongs to the pixel
+ * floor(x/h), floor(y/h)).                                                  */
+static void project_point(const prob_t *P, int is, int js, double xi, double eta, double *u) {
   const refel_t *R = &P->R;
   const int d = R->d;
   memset(u, 0, sizeof(double) * (size_t)P->nx * P->ny * 2 * d);
   for (int t = 0; t < 2; t++) {
+    const double w = xi == eta ? 0.5 : ((t == 0) == (eta < xi) ? 1.0 : 0.0);
+    if (w == 0.0) continue;
     double phi[DMAX];
-    basis(R->p, t, 0.5, 0.5, phi, NULL);
+    basis(R->p, t, xi, eta, phi, NULL);
     double *uT = u + eidx(P, is, js, t);
     for (int a = 0; a < d; a++) {
       double s = 0.0;
       for (int b = 0; b < d; b++) s += R->Minv[t][a][b] * phi[b];
-      uT[a] = 0.5 * s;
+      uT[a] = w * s;
     }
   }
 }
+
+/* the pixel-centre source of P:241 */
+static void project_delta(const prob_t *P, int is, int js, double *u) { project_point(P, is, js, 0.5, 0.5, u); }
 
 /* SSP-RK3 in increment form (reading R7):
  *   U1 = u  + dt L(u)
@@ -466,11 +475,10 @@ static void ssprk3_step(const prob_t *P, double *u, double *U1, double *U2, doub
 /* m_ab = int (x-xs)^a (y-ys)^b u_h, (a,b) in {00,10,01,20,11,02}, exact
  * integration of the DG polynomial by quadrature (reading R14), about the
  * source point xs = pixel centre (reading R12).                             */
-static void moments(const prob_t *P, const double *u, int is, int js, double m[6]) {
+static void moments_about(const prob_t *P, const double *u, double xs, double ys, double m[6]) {
   const refel_t *R = &P->R;
   const int d = R->d;
   const double h = R->h;
-  double xs = (is + 0.5) * h, ys = (js + 0.5) * h;
   for (int k = 0; k < 6; k++) m[k] = 0.0;
   for (int j = 0; j < P->ny; j++)
     for (int i = 0; i < P->nx; i++)
@@ -494,6 +502,10 @@ static void moments(const prob_t *P, const double *u, int is, int js, double m[6
           m[5] += w * Y * Y;
         }
       }
+}
+
+static void moments(const prob_t *P, const double *u, int is, int js, double m[6]) {
+  moments_about(P, u, (is + 0.5) * P->R.h, (js + 0.5) * P->R.h, m);
 }
 
 /* ------------------------------------------------------------------------- */
@@ -630,6 +642,50 @@ int orc_solve(int p, double h, double D, int nx, int ny, const uint8_t *mask, in
       ssprk3_step(P, u, buf + ne, buf + 2 * ne, buf + 3 * ne, buf + 4 * ne, dt);
     double m[6];
     moments(P, u, is, js, m);
+    for (int k = 0; k < 6; k++) {
+      mom_out[s * 6 + k] = m[k];
+      if (!isfinite(m[k])) bad |= 1;
+    }
+    if (dens_out) memcpy(dens_out + (size_t)s * ne, u, sizeof(double) * ne);
+    free(buf);
+  }
+  free(P);
+  return bad ? 4 : 0;
+}
+
+/* orc_solve for point sources anywhere in extracellular pixels (N4):
+ * points [n][2] physical (x, y); pixel (floor(x/h), floor(y/h)) (R21), the
+ * Dirac projected at the point, moments about the point.  Returns as
+ * orc_solve.                                                                */
+int orc_solve_points(int p, double h, double D, int nx, int ny, const uint8_t *mask, int outer_bc,
+                     const double *points, int64_t n, double dt, int64_t nsteps, double *mom_out,
+                     double *dens_out, int nthreads) {
+  prob_t *P = (prob_t *)malloc(sizeof(prob_t));
+  if (setup(P, p, h, D, nx, ny, mask, outer_bc) || n < 0 || nsteps < 0 || !(dt >= 0)) {
+    free(P);
+    return 1;
+  }
+  for (int64_t s = 0; s < n; s++) {
+    double x = points[2 * s] / h, y = points[2 * s + 1] / h;
+    if (!(x >= 0 && y >= 0 && x < nx && y < ny)) { free(P); return 2; }
+    if (mask[(size_t)(int)floor(y) * nx + (int)floor(x)]) { free(P); return 2; }
+  }
+  const size_t ne = (size_t)nx * ny * 2 * P->R.d;
+  int bad = 0;
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 1) reduction(| : bad)
+#endif
+  for (int64_t s = 0; s < n; s++) {
+    double *buf = (double *)malloc(sizeof(double) * 6 * ne);
+    double *u = buf;
+    const double x = points[2 * s] / h, y = points[2 * s + 1] / h;
+    const int is = (int)floor(x), js = (int)floor(y);
+    project_point(P, is, js, x - is, y - js, u);
+    for (int64_t k = 0; k < nsteps; k++)
+      ssprk3_step(P, u, buf + ne, buf + 2 * ne, buf + 3 * ne, buf + 4 * ne, dt);
+    double m[6];
+    moments_about(P, u, points[2 * s], points[2 * s + 1], m);
     for (int k = 0; k < 6; k++) {
       mom_out[s * 6 + k] = m[k];
       if (!isfinite(m[k])) bad |= 1;

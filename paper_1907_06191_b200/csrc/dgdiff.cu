@@ -70,7 +70,8 @@ struct InitVals { double v[2 * DMAXK]; };  // projected Dirac / h^2
 template <typename T, int NV, int D2>
 __global__ void __launch_bounds__(256) k_init_win(T *__restrict__ U, T *__restrict__ Za, T *__restrict__ Zb,
                                                   int nact, const int2 *__restrict__ grange,
-                                                  const int *__restrict__ src_a, InitVals iv) {
+                                                  const int *__restrict__ src_a, InitVals iv,
+                                                  const double *__restrict__ px, int64_t nvalid) {
   constexpr int G = 32 * NV;
   const int g = blockIdx.y;
   const int2 rg = __ldg(&grange[g]);
@@ -85,7 +86,8 @@ __global__ void __launch_bounds__(256) k_init_win(T *__restrict__ U, T *__restri
 #pragma unroll
     for (int e = 0; e < NV; e++) {
       const int s = g * G + lane * NV + e;
-      x[e] = (__ldg(&src_a[s]) == a) ? (T)iv.v[k] : (T)0;
+      const double iv_k = px ? __ldg(&px[min((int64_t)s, nvalid - 1) * (2 + D2) + 2 + k]) : iv.v[k];
+      x[e] = (__ldg(&src_a[s]) == a) ? (T)iv_k : (T)0;
       z[e] = (T)0;
     }
     stv<T, NV>(U + (base + v) * NV, x);
@@ -96,7 +98,9 @@ __global__ void __launch_bounds__(256) k_init_win(T *__restrict__ U, T *__restri
 
 template <typename T, int NV, int D2>
 __global__ void __launch_bounds__(256) k_init(T *__restrict__ U, int64_t nvec, int nact,
-                                              const int *__restrict__ src_a, InitVals iv) {
+                                              const int *__restrict__ src_a, InitVals iv,
+                                              const double *__restrict__ px /* nullable: [nvalid][2 + D2] */,
+                                              int64_t nvalid) {
   constexpr int G = 32 * NV;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec;
        v += (int64_t)gridDim.x * blockDim.x) {
@@ -110,22 +114,24 @@ __global__ void __launch_bounds__(256) k_init(T *__restrict__ U, int64_t nvec, i
 #pragma unroll
     for (int e = 0; e < NV; e++) {
       int s = (int)(g * G + lane * NV + e);
-      x[e] = (__ldg(&src_a[s]) == a) ? (T)iv.v[k] : (T)0;
+      const double iv_k = px ? __ldg(&px[min((int64_t)s, nvalid - 1) * (2 + D2) + 2 + k]) : iv.v[k];
+      x[e] = (__ldg(&src_a[s]) == a) ? (T)iv_k : (T)0;
     }
     stv<T, NV>(U + v * NV, x);
   }
 }
 
 // ---------------------------------------------------------------------------
-// K4: per-source moments about the source pixel centre (readings R12, R14):
+// K4: per-source moments about the source point (readings R12, R14):
 //   m_ab = h^(2+a+b) sum_pixels sum_T sum_j c_j int (xi+X)^a (eta+Y)^b N_j
-// with X = i - is - 1/2, Y = j - js - 1/2.  fp64 accumulation.  Each CTA
+// with X = i - xs, Y = j - ys, (xs, ys) the source point in pixel units (the
+// pixel centre is + 1/2 for pixel sources; N4 sub-pixel points otherwise).  fp64 accumulation.  Each CTA
 // reduces a contiguous pixel range; k_mom_reduce then sums the per-CTA
 // partials in CTA order (deterministic, independent of chunking and ranks).
 // ---------------------------------------------------------------------------
 template <typename T, int NV, int D2>
 __global__ void __launch_bounds__(256) k_moments(const T *__restrict__ U, const int2 *__restrict__ pix,
-                                                 const int2 *__restrict__ src_ij, int nact, int ngroups,
+                                                 const double2 *__restrict__ src_xy, int nact, int ngroups,
                                                  int px_per_cta, double *__restrict__ partial,
                                                  int64_t chunk, const int2 *__restrict__ grange /* nullable (N1) */) {
   constexpr int G = 32 * NV, d = D2 / 2;
@@ -136,9 +142,9 @@ __global__ void __launch_bounds__(256) k_moments(const T *__restrict__ U, const 
   double is[NV], js[NV], m[6][NV];
 #pragma unroll
   for (int e = 0; e < NV; e++) {
-    int2 s = __ldg(&src_ij[g * G + lane * NV + e]);
-    is[e] = s.x + 0.5;
-    js[e] = s.y + 0.5;
+    const double2 s = __ldg(&src_xy[g * G + lane * NV + e]);
+    is[e] = s.x;
+    js[e] = s.y;
 #pragma unroll
     for (int q = 0; q < 6; q++) m[q][e] = 0.0;
   }
@@ -265,15 +271,19 @@ __global__ void k_gather(const T *__restrict__ U, int nact, int g, int slot, dou
 
 // source pixel -> active index for a chunk (padding slots repeat the last
 // valid source, so they never widen an N1 group box)
+// (src_xy = source point in pixel units: the pixel centre, or the N4
+// sub-pixel point from px[k][0..1])
 __global__ void k_src_prep(const int32_t *__restrict__ src, int64_t nvalid, int64_t chunk,
                            const int *__restrict__ aidx, int nx, int *__restrict__ src_a,
-                           int2 *__restrict__ src_ij) {
+                           int2 *__restrict__ src_ij, double2 *__restrict__ src_xy,
+                           const double *__restrict__ px, int pxs) {
   int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= chunk) return;
   int64_t k = s < nvalid ? s : nvalid - 1;
   int i = src[2 * k], j = src[2 * k + 1];
   src_a[s] = aidx[(size_t)j * nx + i];
   src_ij[s] = make_int2(i, j);
+  src_xy[s] = px ? make_double2(px[k * pxs], px[k * pxs + 1]) : make_double2(i + 0.5, j + 0.5);
 }
 
 // ---------------------------------------------------------------------------
@@ -401,6 +411,11 @@ struct dgdiff_s {
   int64_t chunk_cap = 0;  // sources the U buffers hold
   int *d_src_a = nullptr;
   int2 *d_src_ij = nullptr;
+  double2 *d_src_xy = nullptr;   // source points, pixel units (per chunk slot)
+  double *d_px = nullptr;        // N4 sub-pixel sources: [nloc][2 + D2] point + init row (chunk order)
+  int64_t px_cap = 0;
+  bool points = false;           // last solve used sub-pixel points
+  const double *cur_px = nullptr;  // rows of the chunk being solved (points mode)
   double *d_partial = nullptr;
   size_t partial_cap = 0;
   int32_t *d_src = nullptr;
@@ -540,6 +555,8 @@ static void release(dgdiff_s *H) {
   cudaFree(H->d_Aabs);
   cudaFree(H->d_src_a);
   cudaFree(H->d_src_ij);
+  cudaFree(H->d_src_xy);
+  cudaFree(H->d_px);
   cudaFree(H->d_partial);
   cudaFree(H->d_src);
   cudaFree(H->d_mom);
@@ -870,9 +887,9 @@ static dgdiff_status run_chunk(dgdiff_s *H, int64_t nvalid, int64_t chunk, doubl
     // u and the two work registers are (re)initialised over exactly those rows
     dim3 ig((unsigned)std::min<int64_t>(std::max<int64_t>(1, (nvec / std::max(1, ngroups) + 255) / 256), 2048),
             (unsigned)ngroups);
-    k_init_win<T, NV, D2><<<ig, 256, 0, st>>>(u, Ua, Ub, nact, H->d_grange, H->d_src_a, iv);
+    k_init_win<T, NV, D2><<<ig, 256, 0, st>>>(u, Ua, Ub, nact, H->d_grange, H->d_src_a, iv, H->cur_px, nvalid);
   } else {
-    k_init<T, NV, D2><<<blocks, 256, 0, st>>>(u, nvec, nact, H->d_src_a, iv);
+    k_init<T, NV, D2><<<blocks, 256, 0, st>>>(u, nvec, nact, H->d_src_a, iv, H->cur_px, nvalid);
   }
   H->st.launches++;
   // K2 x 3 per step (SSP-RK3 increment form, R7)
@@ -1017,13 +1034,13 @@ after_stepping:
     H->partial_cap = need;
   }
   dim3 mgrid(nblk, (ngroups + wpb - 1) / wpb);
-  k_moments<T, NV, D2><<<mgrid, 32 * wpb, 0, st>>>(u, H->d_pix, H->d_src_ij, nact, ngroups, mpx, H->d_partial,
+  k_moments<T, NV, D2><<<mgrid, 32 * wpb, 0, st>>>(u, H->d_pix, H->d_src_xy, nact, ngroups, mpx, H->d_partial,
                                                chunk, H->windows ? H->d_grange : nullptr);
   k_mom_reduce<<<(int)((nvalid + 127) / 128), 128, 0, st>>>(H->d_partial, nblk, chunk, nvalid, H->h, mom_rows,
                                                             H->windows ? H->d_perm + H->last_chunk_pos0 : nullptr,
                                                             H->d_mom);
   H->st.launches += 2;
-  if (H->mix_R > 0) {
+  if (H->mix_R > 0 && !H->points) {   // the lattice is defined about pixel-centre sources (R20)
     const int nc = (2 * H->mix_R + 1) * (2 * H->mix_R + 1);
     k_mixture<T, NV, D2><<<(nc + 127) / 128, 128, 0, st>>>(u, H->d_aidx, H->nx, H->ny, nact, H->d_src_ij, mom_rows,
                                                          nvalid, H->mix_R, H->d_mix,
@@ -1055,8 +1072,10 @@ static dgdiff_status run_chunk_p(dgdiff_s *H, int64_t nvalid, int64_t chunk, dou
   return fail(DGDIFF_E_ARG, "internal: lane width");
 }
 
-extern "C" dgdiff_status dgdiff_solve_batch(dgdiff_t H, const int32_t *sources, int64_t n, double dt,
-                                            int64_t nsteps) {
+// sources: [n][2] pixel (i, j); px: nullable [n][2 + D2] sub-pixel points
+// (pixel units) and their projected-Dirac rows (N4), in the same order
+static dgdiff_status solve_impl(dgdiff_s *H, const int32_t *sources, const double *px, int64_t n, double dt,
+                                int64_t nsteps) {
   if (!H) return fail(DGDIFF_E_ARG, "handle is NULL");
   if (n < 1 || !sources) return fail(DGDIFF_E_ARG, "need n >= 1 sources");
   if (n >= (1LL << 31)) return fail(DGDIFF_E_ARG, "too many sources");
@@ -1102,6 +1121,8 @@ extern "C" dgdiff_status dgdiff_solve_batch(dgdiff_t H, const int32_t *sources, 
   CK(cudaMemcpyAsync(H->d_src, sources, sizeof(int32_t) * 2 * n, cudaMemcpyHostToDevice, H->stream));
   H->st.h2d_bytes += sizeof(int32_t) * 2 * n;
   std::vector<int32_t> srt;   // N1: this rank's sources in Morton order
+  std::vector<int64_t> ord(std::max<int64_t>(nloc, 0));   // chunk order -> local index
+  for (int64_t k = 0; k < nloc; k++) ord[k] = k;
   if (nloc > 0 && H->windows) {
     auto morton = [](uint32_t x, uint32_t y) {
       uint64_t k = 0;
@@ -1109,8 +1130,6 @@ extern "C" dgdiff_status dgdiff_solve_batch(dgdiff_t H, const int32_t *sources, 
         k |= (uint64_t)((x >> bit) & 1) << (2 * bit) | (uint64_t)((y >> bit) & 1) << (2 * bit + 1);
       return k;
     };
-    std::vector<int64_t> ord(nloc);
-    for (int64_t k = 0; k < nloc; k++) ord[k] = k;
     std::stable_sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) {
       return morton(sources[2 * (b + x)], sources[2 * (b + x) + 1]) <
              morton(sources[2 * (b + y)], sources[2 * (b + y) + 1]);
@@ -1135,6 +1154,22 @@ extern "C" dgdiff_status dgdiff_solve_batch(dgdiff_t H, const int32_t *sources, 
     CK(cudaMemcpyAsync(H->d_perm, perm.data(), sizeof(int32_t) * nloc, cudaMemcpyHostToDevice, H->stream));
     H->st.h2d_bytes += sizeof(int32_t) * 3 * nloc;
   }
+  // N4 sub-pixel points: point + projected-Dirac row per source, chunk order
+  const int PXS = 2 + H->D2;
+  H->points = px != nullptr;
+  if (nloc > 0 && px) {
+    std::vector<double> rows((size_t)nloc * PXS);
+    for (int64_t k = 0; k < nloc; k++)
+      memcpy(&rows[(size_t)k * PXS], px + (size_t)(b + ord[k]) * PXS, sizeof(double) * PXS);
+    if (nloc > H->px_cap) {
+      cudaFree(H->d_px);
+      H->d_px = nullptr;
+      CK(cudaMalloc(&H->d_px, sizeof(double) * PXS * nloc));
+      H->px_cap = nloc;
+    }
+    CK(cudaMemcpyAsync(H->d_px, rows.data(), sizeof(double) * PXS * nloc, cudaMemcpyHostToDevice, H->stream));
+    H->st.h2d_bytes += sizeof(double) * PXS * nloc;
+  }
   if (nloc > 0) {
     // chunk size: fit 3 RK registers in free device memory
     const size_t per_src = 3 * (size_t)H->nact * H->D2 * tsize(H);
@@ -1147,6 +1182,7 @@ extern "C" dgdiff_status dgdiff_solve_batch(dgdiff_t H, const int32_t *sources, 
       for (int r = 0; r < 3; r++) H->d_U[r] = nullptr;
       cudaFree(H->d_src_a); H->d_src_a = nullptr;
       cudaFree(H->d_src_ij); H->d_src_ij = nullptr;
+      cudaFree(H->d_src_xy); H->d_src_xy = nullptr;
       H->chunk_cap = 0;
       size_t fr = 0, tot = 0;
       CK(cudaMemGetInfo(&fr, &tot));
@@ -1163,6 +1199,7 @@ extern "C" dgdiff_status dgdiff_solve_batch(dgdiff_t H, const int32_t *sources, 
       }
       CK(cudaMalloc(&H->d_src_a, sizeof(int) * chunk));
       CK(cudaMalloc(&H->d_src_ij, sizeof(int2) * chunk));
+      CK(cudaMalloc(&H->d_src_xy, sizeof(double2) * chunk));
       H->chunk_cap = chunk;
     } else {
       chunk = std::min(chunk, H->chunk_cap);
@@ -1172,8 +1209,10 @@ extern "C" dgdiff_status dgdiff_solve_batch(dgdiff_t H, const int32_t *sources, 
       int64_t nvalid = std::min(chunk, nloc - c0);
       int64_t cpad = (nvalid + G - 1) / G * G;
       const int32_t *srcp = H->windows ? H->d_srcw + 2 * c0 : H->d_src + 2 * (b + c0);
+      H->cur_px = px ? H->d_px + (size_t)c0 * PXS : nullptr;
       k_src_prep<<<(int)((cpad + 127) / 128), 128, 0, H->stream>>>(srcp, nvalid, cpad, H->d_aidx, H->nx,
-                                                                 H->d_src_a, H->d_src_ij);
+                                                                 H->d_src_a, H->d_src_ij, H->d_src_xy,
+                                                                 H->cur_px, PXS);
       H->st.launches++;
       double *rows = H->d_mom + 6 * (b + c0);
       if (H->windows) {
@@ -1233,6 +1272,37 @@ extern "C" dgdiff_status dgdiff_solve_batch(dgdiff_t H, const int32_t *sources, 
   return DGDIFF_OK;
 }
 
+extern "C" dgdiff_status dgdiff_solve_batch(dgdiff_t H, const int32_t *sources, int64_t n, double dt,
+                                            int64_t nsteps) {
+  return solve_impl(H, sources, nullptr, n, dt, nsteps);
+}
+
+extern "C" dgdiff_status dgdiff_solve_batch_points(dgdiff_t H, const double *points, int64_t n, double dt,
+                                                   int64_t nsteps) {
+  if (!H) return fail(DGDIFF_E_ARG, "handle is NULL");
+  if (n < 1 || !points) return fail(DGDIFF_E_ARG, "need n >= 1 points");
+  if (n >= (1LL << 31)) return fail(DGDIFF_E_ARG, "too many sources");
+  const int PXS = 2 + H->D2;
+  std::vector<int32_t> pix((size_t)2 * n);
+  std::vector<double> px((size_t)n * PXS);
+  for (int64_t s = 0; s < n; s++) {
+    const double x = points[2 * s] / H->h, y = points[2 * s + 1] / H->h;   // pixel units
+    if (!std::isfinite(x) || !std::isfinite(y) || x < 0 || y < 0 || x >= H->nx || y >= H->ny)
+      return fail(DGDIFF_E_SOURCE, "point %lld (%.17g, %.17g) is outside the grid", (long long)s, points[2 * s],
+                  points[2 * s + 1]);
+    const int i = std::min(H->nx - 1, (int)std::floor(x)), j = std::min(H->ny - 1, (int)std::floor(y));
+    pix[2 * s] = i;
+    pix[2 * s + 1] = j;
+    double *r = &px[(size_t)s * PXS];
+    r[0] = x;
+    r[1] = y;
+    dgop::point_init(H->tab, x - i, y - j, r + 2);
+    const double ih2 = 1.0 / (H->h * H->h);
+    for (int k = 0; k < H->D2; k++) r[2 + k] *= ih2;
+  }
+  return solve_impl(H, pix.data(), px.data(), n, dt, nsteps);
+}
+
 extern "C" dgdiff_status dgdiff_covariance(dgdiff_t H, double delta, double sigma[4], double mu[2]) {
   if (!H) return fail(DGDIFF_E_ARG, "handle is NULL");
   if (!sigma) return fail(DGDIFF_E_ARG, "sigma is NULL");
@@ -1278,6 +1348,7 @@ extern "C" dgdiff_status dgdiff_mixture(dgdiff_t H, double *grid, double *residu
   if (!H) return fail(DGDIFF_E_ARG, "handle is NULL");
   if (H->mix_R <= 0) return fail(DGDIFF_E_STATE, "create the handle with opts.mixture_radius > 0");
   if (!H->solved || !H->have_sigma) return fail(DGDIFF_E_STATE, "dgdiff_mixture needs dgdiff_covariance first");
+  if (H->points) return fail(DGDIFF_E_STATE, "the mixture lattice is defined for pixel-centre sources (dgdiff_solve_batch)");
   CK(cudaSetDevice(H->dev));
   const int R = H->mix_R;
   const size_t nc = (size_t)(2 * R + 1) * (2 * R + 1);

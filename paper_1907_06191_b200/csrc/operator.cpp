@@ -380,7 +380,38 @@ Table build(int p) {
   T.cw.assign((size_t)2 * d, 0.0);
   for (int t = 0; t < 2; t++)
     for (int j = 0; j < d; j++) T.cw[t * d + j] = peval(R.phi[t][j], Q(1, 2), Q(1, 2)).to_double();
+  // M^-1 and the monomial coefficients of the basis, for sub-pixel Diracs
+  T.minv.assign((size_t)2 * d * d, 0.0);
+  T.phic.assign((size_t)2 * d * (p + 1) * (p + 1), 0.0);
+  for (int t = 0; t < 2; t++)
+    for (int i = 0; i < d; i++) {
+      for (int j = 0; j < d; j++) T.minv[((size_t)t * d + i) * d + j] = R.Minv[t][i][j].to_double();
+      for (int a = 0; a <= p; a++)
+        for (int b = 0; b <= p; b++)
+          T.phic[(((size_t)t * d + i) * (p + 1) + a) * (p + 1) + b] = R.phi[t][i][a][b].to_double();
+    }
   return T;
+}
+
+void point_init(const Table &T, double xi, double eta, double *out) {
+  const int p = T.p, d = T.d;
+  const double wt[2] = {eta < xi ? 1.0 : eta > xi ? 0.0 : 0.5, eta > xi ? 1.0 : eta < xi ? 0.0 : 0.5};
+  for (int t = 0; t < 2; t++) {
+    double phi[16];
+    for (int j = 0; j < d; j++) {
+      double s = 0.0, xa = 1.0;
+      for (int a = 0; a <= p; a++, xa *= xi) {
+        double yb = 1.0;
+        for (int b = 0; b <= p; b++, yb *= eta) s += T.phic[(((size_t)t * d + j) * (p + 1) + a) * (p + 1) + b] * xa * yb;
+      }
+      phi[j] = s;
+    }
+    for (int i = 0; i < d; i++) {
+      double s = 0.0;
+      for (int j = 0; j < d; j++) s += T.minv[((size_t)t * d + i) * d + j] * phi[j];
+      out[t * d + i] = wt[t] * s;
+    }
+  }
 }
 
 std::vector<double> build_absorb(int p) {

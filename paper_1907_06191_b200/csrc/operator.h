@@ -11,7 +11,15 @@ struct Table {
   std::vector<double> init; // [2][d] projected Dirac at the pixel centre, units 1/h^2
   std::vector<int> nnz;     // [16][5] structural non-zeros per block
   std::vector<double> cw;   // [2][d] N_j at the pixel centre (1/2, 1/2) (mixture node values)
+  std::vector<double> minv; // [2][d][d] M_T^-1 on the unit pixel (rounded from exact)
+  std::vector<double> phic; // [2][d][p+1][p+1] monomial coefficients of N_j (xi^a eta^b)
 };
+
+// Projected Dirac at the pixel-local point (xi, eta) in [0,1)^2 (N4 sub-pixel
+// sources; generalises reading R10): u_T = w_T M_T^-1 N_T(xi, eta), w = 1 on
+// the triangle containing the point (L: eta < xi, U: eta > xi), 1/2 on each
+// if it lies on the diagonal.  out[2][d], units 1/h^2.
+void point_init(const Table &T, double xi, double eta, double *out);
 
 // Throws std::runtime_error on failure (unsupported degree, non-dyadic entry,
 // non-zero corner coupling, rational overflow).

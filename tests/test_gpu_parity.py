@@ -593,3 +593,60 @@ def test_p3_random_masks_and_free_space(dg, orc, prec):
         s.solve(np.array([[48, 48], [47, 49], [49, 47]], np.int32), 1 / 256, 256)
         S, mu = s.covariance()
     assert np.abs(S - 2.0 * np.eye(2)).max() <= (1e-11 if prec == 64 else 2e-4)
+
+
+@pytest.mark.parametrize("p,prec,windows", [(1, 64, 0), (1, 32, 0), (2, 64, 0), (1, 64, 1), (3, 64, 0)])
+def test_subpixel_points_vs_oracle(dg, orc, p, prec, windows):
+    """N4 sub-pixel sources: points inside L, inside U, on the diagonal and on
+    pixel edges (R21), a ragged two-chunk batch, against O1's solve_points
+    (densities of the kept chunk, per-source moments about the point, Sigma)."""
+    rng = np.random.default_rng(500 + 10 * p + prec + windows)
+    ny, nx = 22, 26
+    m = (rng.random((ny, nx)) < 0.35).astype(np.uint8)
+    free = np.argwhere(m == 0)
+    G = {1: 64, 2: 32, 3: 32}[p] * (2 if prec == 32 else 1)
+    n = G + 9
+    pick = free[rng.integers(0, len(free), n)]
+    loc = rng.random((n, 2))
+    loc[0] = (0.3, 0.3)        # diagonal
+    loc[1] = (0.0, 0.6)        # left edge
+    loc[2] = (0.45, 0.0)       # bottom edge
+    loc[3] = (0.5, 0.5)        # centre
+    h = 0.8
+    pts = (np.stack([pick[:, 1], pick[:, 0]], 1) + loc) * h
+    dt = {1: 1 / 32, 2: 1 / 128, 3: 1 / 256}[p] * h * h / 1.3
+    ref_m, ref_d = orc.solve_points(p, h, 1.3, m, pts, dt, 30, keep_density=True)
+    with dg.Solver(m, h, 1.3, p, precision=prec, keep_density=1, max_chunk=G, windows=windows) as s:
+        s.solve_points(pts, dt, 30)
+        S, mu = s.covariance()
+        mom = s.moments()
+        dens = {k: s.density(k) for k in range(n) if _in_last_chunk(s, k)}
+    t = TOL[prec]
+    assert len(dens) == n - G
+    for k, dk in dens.items():
+        assert rel_l2(dk, ref_d[k]) <= t["dens"], k
+    assert mom_err(mom, ref_m) <= t["mom"]
+    R, _ = orc.sigma(ref_m)
+    assert sig_err(S, R) <= t["sig"]
+
+
+def test_points_at_centres_equal_pixel_sources(dg, cfg):
+    """dgdiff_solve_batch_points at pixel centres == dgdiff_solve_batch, bitwise;
+    out-of-grid / axon points are E_SOURCE; the mixture is refused."""
+    m = cfg.mask("c3")
+    src = cfg.sources("c3")[:100]
+    with dg.Solver(m, 1.0, 1.0, 1, mixture_radius=4) as s:
+        s.solve(src, 1 / 32, 20)
+        a = s.moments()
+        s.solve_points(src + 0.5, 1 / 32, 20)
+        b = s.moments()
+        s.covariance()
+        with pytest.raises(dg.DGDiffError) as e:
+            s.mixture()
+        assert e.value.status == dg.E_STATE
+        axon = np.argwhere(m == 1)[0][::-1] + 0.5
+        for bad in ([[-0.1, 3.0]], [[512.0, 3.0]], [axon], [[np.nan, 1.0]]):
+            with pytest.raises(dg.DGDiffError) as e:
+                s.solve_points(np.array(bad, float), 1 / 32, 2)
+            assert e.value.status == dg.E_SOURCE
+    assert np.array_equal(a, b)

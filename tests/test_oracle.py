@@ -469,3 +469,44 @@ def test_mixture_translation_invariance_p1(orc):
     g = orc.mixture(1, dens, src, mom, 10)
     g1 = orc.mixture(1, dens[:1], src[:1], mom[:1], 10)
     assert np.abs(g - g1).max() <= 1e-12 * g1.max()
+
+
+# ---------------------------------------------------------------- N4 sub-pixel point sources
+def test_points_reduce_to_pixel_centres(orc):
+    """A point at a pixel centre is the pixel source of P:241 (bitwise)."""
+    mask, src = _case(31)
+    pts = [(i + 0.5, j + 0.5) for i, j in src]
+    assert np.array_equal(orc.solve_points(1, 1.0, 1.0, mask, pts, 1 / 32, 20), orc.solve(1, 1.0, 1.0, mask, src, 1 / 32, 20))
+
+
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_point_projection_moments_exact(orc, p):
+    """The L2 projection onto P_p reproduces every moment of degree <= p:
+    mass 1 and first moments 0 about the point for any p, and (p >= 2) the
+    second moments 0 too.  Points inside L, inside U, on the diagonal and on
+    the pixel's lower-left edges (R21).  Catches a wrong triangle choice, a
+    basis evaluated at the wrong local point, or moments about the pixel
+    centre instead of the point."""
+    m = np.zeros((6, 6), np.uint8)
+    h = 0.7
+    pts = [(2.71 * h, 3.22 * h), (2.23 * h, 3.64 * h), (2.4 * h, 3.4 * h), (2.0 * h, 3.3 * h), (2.6 * h, 3.0 * h)]
+    mom = orc.solve_points(p, h, 1.0, m, pts, 1e-3, 0)
+    assert np.allclose(mom[:, 0], 1.0, rtol=0, atol=1e-13)
+    assert np.abs(mom[:, 1:3]).max() <= 1e-13
+    if p >= 2:
+        assert np.abs(mom[:, 3:]).max() <= 1e-13
+    else:
+        assert np.abs(mom[:, 3:]).max() > 1e-4          # P1 cannot hold x^2: a real test above
+
+
+def test_point_free_space_p2_closed_form_and_translation(orc):
+    """Free space, P2: Sigma = 2 D Delta I for a source anywhere in a pixel
+    (the closed form does not depend on where the Dirac sits), and a shift by
+    one whole pixel leaves every moment unchanged (the mesh is translation
+    invariant by whole pixels)."""
+    m = np.zeros((76, 76), np.uint8)                      # walls >= 25 sigma away
+    pts = [(37.31, 37.77), (38.31, 37.77)]
+    mom = orc.solve_points(2, 1.0, 1.0, m, pts, 1 / 128, 128)
+    S, _ = orc.sigma(mom[:1])
+    assert np.abs(S - 2.0 * np.eye(2)).max() <= 1e-12
+    assert np.allclose(mom[0], mom[1], rtol=0, atol=1e-12)
