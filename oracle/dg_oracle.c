@@ -839,3 +839,336 @@ int orc_residual(const double *grid, int R, double h, const double *sigma, const
   *res = r;
   return 0;
 }
+
+/* ========================================================================= */
+/* N4: quadrilateral Q_p elements, one per pixel (SURVEY 8f "Q_p elements on  */
+/* one-pixel cells", the north star's "Q2").  The same mixed system, fluxes   */
+/* and readings as the triangles (Eq. (7), R4-R7, R9 REFLECT),    */
+/* with the tensor-product Lagrange basis N_ab(xi, eta) = l_a(xi) l_b(eta) on */
+/* the equispaced nodes (a/p, b/p), dof k = b (p+1) + a, and four faces      */
+/* E, W, N, S (bit order of the open-face code).  Written out element by     */
+/* element like the triangle oracle: a q pass, then an rhs pass.             */
+/* ========================================================================= */
+#define QDMAX 16 /* (p+1)^2 for p <= 3 */
+
+typedef struct {
+  int p, d;
+  double h;
+  double M[QDMAX][QDMAX], Minv[QDMAX][QDMAX];
+  double Dc[2][QDMAX][QDMAX];
+  double Em[4][QDMAX][QDMAX], Ep[4][QDMAX][QDMAX];
+  int nq;
+  double qx[QMAX * QMAX][2], qw[QMAX * QMAX];
+} qref_t;
+
+static const int QNB[4][2] = {{1, 0}, {-1, 0}, {0, 1}, {0, -1}};   /* E W N S */
+static const double QNRM[4][2] = {{1, 0}, {-1, 0}, {0, 1}, {0, -1}};
+
+/* 1-D Lagrange basis on s_k = k/p and its derivative */
+static void lag1(int p, double s, double *l, double *dl) {
+  for (int a = 0; a <= p; a++) {
+    double v = 1.0, dv = 0.0;
+    for (int k = 0; k <= p; k++) {
+      if (k == a) continue;
+      const double den = (double)(a - k) / p;
+      /* product rule: d(v * (s - s_k)/den) */
+      dv = dv * (s - (double)k / p) / den + v / den;
+      v *= (s - (double)k / p) / den;
+    }
+    l[a] = v;
+    if (dl) dl[a] = dv;
+  }
+}
+
+static void qbasis(int p, double xi, double eta, double *phi, double (*g)[2]) {
+  double lx[4], dlx[4], ly[4], dly[4];
+  lag1(p, xi, lx, dlx);
+  lag1(p, eta, ly, dly);
+  for (int b = 0; b <= p; b++)
+    for (int a = 0; a <= p; a++) {
+      const int k = b * (p + 1) + a;
+      phi[k] = lx[a] * ly[b];
+      if (g) { g[k][0] = dlx[a] * ly[b]; g[k][1] = lx[a] * dly[b]; }
+    }
+}
+
+static void qinvert(int d, double A[QDMAX][QDMAX], double X[QDMAX][QDMAX]) {
+  double a[QDMAX][2 * QDMAX];
+  for (int i = 0; i < d; i++)
+    for (int j = 0; j < 2 * d; j++) a[i][j] = (j < d) ? A[i][j] : (j - d == i ? 1.0 : 0.0);
+  for (int c = 0; c < d; c++) {
+    int piv = c;
+    for (int r = c + 1; r < d; r++)
+      if (fabs(a[r][c]) > fabs(a[piv][c])) piv = r;
+    if (piv != c)
+      for (int j = 0; j < 2 * d; j++) { double tmp = a[c][j]; a[c][j] = a[piv][j]; a[piv][j] = tmp; }
+    double s = 1.0 / a[c][c];
+    for (int j = 0; j < 2 * d; j++) a[c][j] *= s;
+    for (int r = 0; r < d; r++)
+      if (r != c) {
+        double f = a[r][c];
+        if (f != 0.0)
+          for (int j = 0; j < 2 * d; j++) a[r][j] -= f * a[c][j];
+      }
+  }
+  for (int i = 0; i < d; i++)
+    for (int j = 0; j < d; j++) X[i][j] = a[i][d + j];
+}
+
+static void qref_init(qref_t *R, int p, double h) {
+  memset(R, 0, sizeof(*R));
+  R->p = p;
+  R->d = (p + 1) * (p + 1);
+  R->h = h;
+  const int d = R->d, n = p + 2;   /* tensor Gauss, exact to degree 2p+2 per direction */
+  double gx[QMAX], gw[QMAX];
+  gauss_legendre01(n, gx, gw);
+  R->nq = n * n;
+  for (int iy = 0, q = 0; iy < n; iy++)
+    for (int ix = 0; ix < n; ix++, q++) {
+      R->qx[q][0] = gx[ix];
+      R->qx[q][1] = gx[iy];
+      R->qw[q] = gw[ix] * gw[iy] * h * h;
+    }
+  for (int q = 0; q < R->nq; q++) {
+    double phi[QDMAX], g[QDMAX][2];
+    qbasis(p, R->qx[q][0], R->qx[q][1], phi, g);
+    for (int i = 0; i < d; i++)
+      for (int j = 0; j < d; j++) {
+        R->M[i][j] += R->qw[q] * phi[i] * phi[j];
+        for (int c = 0; c < 2; c++) R->Dc[c][i][j] += R->qw[q] * (g[i][c] / h) * phi[j];
+      }
+  }
+  qinvert(d, R->M, R->Minv);
+  /* faces: the point s along the face; K's local point and the neighbour's */
+  for (int f = 0; f < 4; f++)
+    for (int k = 0; k < n; k++) {
+      const double s = gx[k];
+      double xk, yk;
+      if (f == 0) { xk = 1; yk = s; } else if (f == 1) { xk = 0; yk = s; }
+      else if (f == 2) { xk = s; yk = 1; } else { xk = s; yk = 0; }
+      double pm[QDMAX], pp[QDMAX];
+      qbasis(p, xk, yk, pm, NULL);
+      qbasis(p, xk - QNB[f][0], yk - QNB[f][1], pp, NULL);
+      const double w = gw[k] * h;
+      for (int i = 0; i < d; i++)
+        for (int j = 0; j < d; j++) {
+          R->Em[f][i][j] += w * pm[i] * pm[j];
+          R->Ep[f][i][j] += w * pm[i] * pp[j];
+        }
+    }
+}
+
+typedef struct {
+  qref_t R;
+  int nx, ny;
+  double D;
+  const uint8_t *mask;
+} qprob_t;
+
+static double qkpix(const qprob_t *P, int i, int j) {
+  if (i < 0 || j < 0 || i >= P->nx || j >= P->ny) return 0.0;   /* REFLECT (R9) */
+  return P->mask[(size_t)j * P->nx + i] ? 0.0 : P->D;
+}
+
+static inline size_t qidx(const qprob_t *P, int i, int j) { return ((size_t)j * P->nx + i) * P->R.d; }
+
+/* Lu = M^-1 [rhs of Eq. (7)] for Q_p: q pass, then rhs pass */
+static void q_apply_L(const qprob_t *P, const double *u, double *q, double *Lu) {
+  const qref_t *R = &P->R;
+  const int d = R->d, nx = P->nx, ny = P->ny;
+  const size_t nel = (size_t)nx * ny * d;
+  double *qx = q, *qy = q + nel;
+  static const double zero[QDMAX] = {0};
+  for (int j = 0; j < ny; j++)
+    for (int i = 0; i < nx; i++) {
+      const double *uK = u + qidx(P, i, j);
+      double r[2][QDMAX];
+      for (int c = 0; c < 2; c++)
+        for (int a = 0; a < d; a++) {
+          double s = 0.0;
+          for (int b = 0; b < d; b++) s -= R->Dc[c][a][b] * uK[b];
+          r[c][a] = s;
+        }
+      for (int f = 0; f < 4; f++) {
+        const int in = i + QNB[f][0], jn = j + QNB[f][1];
+        const int outside = (in < 0 || jn < 0 || in >= nx || jn >= ny);
+        const double *un = outside ? zero : u + qidx(P, in, jn);   /* u+ = 0 outside (R6, R9) */
+        for (int a = 0; a < d; a++) {
+          double s = 0.0;
+          for (int b = 0; b < d; b++) s += R->Em[f][a][b] * uK[b] + R->Ep[f][a][b] * un[b];
+          s *= 0.5;
+          r[0][a] += QNRM[f][0] * s;
+          r[1][a] += QNRM[f][1] * s;
+        }
+      }
+      for (int a = 0; a < d; a++) {
+        double sx = 0.0, sy = 0.0;
+        for (int b = 0; b < d; b++) {
+          sx += R->Minv[a][b] * r[0][b];
+          sy += R->Minv[a][b] * r[1][b];
+        }
+        qx[qidx(P, i, j) + a] = sx;
+        qy[qidx(P, i, j) + a] = sy;
+      }
+    }
+  for (int j = 0; j < ny; j++)
+    for (int i = 0; i < nx; i++) {
+      const double kK = qkpix(P, i, j);
+      const double *qK[2] = {qx + qidx(P, i, j), qy + qidx(P, i, j)};
+      double r[QDMAX];
+      for (int a = 0; a < d; a++) {
+        double s = 0.0;
+        for (int c = 0; c < 2; c++)
+          for (int b = 0; b < d; b++) s += R->Dc[c][a][b] * qK[c][b];
+        r[a] = -kK * s;
+      }
+      for (int f = 0; f < 4; f++) {
+        const int in = i + QNB[f][0], jn = j + QNB[f][1];
+        const double kf = harmonic(kK, qkpix(P, in, jn));
+        if (kf == 0.0) continue;
+        const double *qN[2] = {qx + qidx(P, in, jn), qy + qidx(P, in, jn)};
+        for (int a = 0; a < d; a++) {
+          double s = 0.0;
+          for (int c = 0; c < 2; c++) {
+            double sc = 0.0;
+            for (int b = 0; b < d; b++) sc += R->Em[f][a][b] * qK[c][b] + R->Ep[f][a][b] * qN[c][b];
+            s += QNRM[f][c] * sc;
+          }
+          r[a] += kf * 0.5 * s;
+        }
+      }
+      for (int a = 0; a < d; a++) {
+        double s = 0.0;
+        for (int b = 0; b < d; b++) s += R->Minv[a][b] * r[b];
+        Lu[qidx(P, i, j) + a] = s;
+      }
+    }
+}
+
+static void q_ssprk3_step(const qprob_t *P, double *u, double *U1, double *U2, double *Lb, double *q, double dt) {
+  const size_t n = (size_t)P->nx * P->ny * P->R.d;
+  q_apply_L(P, u, q, Lb);
+  for (size_t k = 0; k < n; k++) U1[k] = u[k] + dt * Lb[k];
+  q_apply_L(P, U1, q, Lb);
+  for (size_t k = 0; k < n; k++) U2[k] = U1[k] + 0.75 * (u[k] - U1[k]) + 0.25 * dt * Lb[k];
+  q_apply_L(P, U2, q, Lb);
+  for (size_t k = 0; k < n; k++) u[k] = U2[k] + (1.0 / 3.0) * (u[k] - U2[k]) + (2.0 / 3.0) * dt * Lb[k];
+}
+
+/* Dirac at the centre of pixel (is, js): M u_K = N(1/2, 1/2) (interior point:
+ * no split) */
+static void q_project_delta(const qprob_t *P, int is, int js, double *u) {
+  const qref_t *R = &P->R;
+  memset(u, 0, sizeof(double) * (size_t)P->nx * P->ny * R->d);
+  double phi[QDMAX];
+  qbasis(R->p, 0.5, 0.5, phi, NULL);
+  double *uK = u + qidx(P, is, js);
+  for (int a = 0; a < R->d; a++) {
+    double s = 0.0;
+    for (int b = 0; b < R->d; b++) s += R->Minv[a][b] * phi[b];
+    uK[a] = s;
+  }
+}
+
+static void q_moments(const qprob_t *P, const double *u, int is, int js, double m[6]) {
+  const qref_t *R = &P->R;
+  const double h = R->h, xs = (is + 0.5) * h, ys = (js + 0.5) * h;
+  for (int k = 0; k < 6; k++) m[k] = 0.0;
+  for (int j = 0; j < P->ny; j++)
+    for (int i = 0; i < P->nx; i++) {
+      const double *uK = u + qidx(P, i, j);
+      int nz = 0;
+      for (int a = 0; a < R->d; a++) nz |= (uK[a] != 0.0);
+      if (!nz) continue;
+      for (int q = 0; q < R->nq; q++) {
+        double phi[QDMAX];
+        qbasis(R->p, R->qx[q][0], R->qx[q][1], phi, NULL);
+        double val = 0.0;
+        for (int a = 0; a < R->d; a++) val += uK[a] * phi[a];
+        const double X = (i + R->qx[q][0]) * h - xs, Y = (j + R->qx[q][1]) * h - ys, w = R->qw[q] * val;
+        m[0] += w;
+        m[1] += w * X;
+        m[2] += w * Y;
+        m[3] += w * X * X;
+        m[4] += w * X * Y;
+        m[5] += w * Y * Y;
+      }
+    }
+}
+
+static int q_setup(qprob_t *P, int p, double h, double D, int nx, int ny, const uint8_t *mask) {
+  if (p < 1 || p > 3 || !(h > 0) || !(D > 0) || nx < 1 || ny < 1 || !mask) return 1;
+  qref_init(&P->R, p, h);
+  P->nx = nx;
+  P->ny = ny;
+  P->D = D;
+  P->mask = mask;
+  return 0;
+}
+
+/* reference matrices: M, Minv [d][d]; Dc [2][d][d]; Em, Ep [4][d][d] */
+int orc_q_reference(int p, double h, double *M, double *Minv, double *Dc, double *Em, double *Ep) {
+  if (p < 1 || p > 3) return 1;
+  qref_t *R = (qref_t *)malloc(sizeof(qref_t));
+  qref_init(R, p, h);
+  const int d = R->d;
+  for (int i = 0; i < d; i++)
+    for (int j = 0; j < d; j++) {
+      M[i * d + j] = R->M[i][j];
+      Minv[i * d + j] = R->Minv[i][j];
+      for (int c = 0; c < 2; c++) Dc[(c * d + i) * d + j] = R->Dc[c][i][j];
+      for (int f = 0; f < 4; f++) {
+        Em[(f * d + i) * d + j] = R->Em[f][i][j];
+        Ep[(f * d + i) * d + j] = R->Ep[f][i][j];
+      }
+    }
+  free(R);
+  return 0;
+}
+
+/* u, out: [ny][nx][(p+1)^2] */
+int orc_q_apply_L(int p, double h, double D, int nx, int ny, const uint8_t *mask, const double *u, double *out) {
+  qprob_t *P = (qprob_t *)malloc(sizeof(qprob_t));
+  if (q_setup(P, p, h, D, nx, ny, mask)) { free(P); return 1; }
+  double *q = (double *)malloc(sizeof(double) * 2 * (size_t)nx * ny * P->R.d);
+  q_apply_L(P, u, q, out);
+  free(q);
+  free(P);
+  return 0;
+}
+
+/* as orc_solve (REFLECT), for Q_p; dens_out: NULL or [n][ny][nx][(p+1)^2] */
+int orc_q_solve(int p, double h, double D, int nx, int ny, const uint8_t *mask, const int32_t *sources, int64_t n,
+                double dt, int64_t nsteps, double *mom_out, double *dens_out, int nthreads) {
+  qprob_t *P = (qprob_t *)malloc(sizeof(qprob_t));
+  if (q_setup(P, p, h, D, nx, ny, mask) || n < 0 || nsteps < 0 || !(dt >= 0)) { free(P); return 1; }
+  for (int64_t s = 0; s < n; s++) {
+    int is = sources[2 * s], js = sources[2 * s + 1];
+    if (is < 0 || js < 0 || is >= nx || js >= ny || mask[(size_t)js * nx + is]) { free(P); return 2; }
+  }
+  const size_t ne = (size_t)nx * ny * P->R.d;
+  int bad = 0;
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 1) reduction(| : bad)
+#endif
+  for (int64_t s = 0; s < n; s++) {
+    double *buf = (double *)malloc(sizeof(double) * 6 * ne);
+    double *u = buf;
+    const int is = sources[2 * s], js = sources[2 * s + 1];
+    q_project_delta(P, is, js, u);
+    for (int64_t k = 0; k < nsteps; k++)
+      q_ssprk3_step(P, u, buf + ne, buf + 2 * ne, buf + 3 * ne, buf + 4 * ne, dt);
+    double m[6];
+    q_moments(P, u, is, js, m);
+    for (int k = 0; k < 6; k++) {
+      mom_out[s * 6 + k] = m[k];
+      if (!isfinite(m[k])) bad |= 1;
+    }
+    if (dens_out) memcpy(dens_out + (size_t)s * ne, u, sizeof(double) * ne);
+    free(buf);
+  }
+  free(P);
+  return bad ? 4 : 0;
+}

@@ -52,6 +52,10 @@ def lib():
         L.orc_solve.argtypes = [c_int, c_double, c_double, c_int, c_int, _u8p, c_int, _i32p, c_i64,
                                 c_double, c_i64, _dp, _dp, c_int]
         L.orc_sigma.argtypes = [_dp, c_i64, c_int, _dp, _dp]
+        L.orc_q_reference.argtypes = [c_int, c_double] + [_dp] * 5
+        L.orc_q_apply_L.argtypes = [c_int, c_double, c_double, c_int, c_int, _u8p, _dp, _dp]
+        L.orc_q_solve.argtypes = [c_int, c_double, c_double, c_int, c_int, _u8p, _i32p, c_i64, c_double, c_i64,
+                                  _dp, _dp, c_int]
         L.orc_solve_points.argtypes = [c_int, c_double, c_double, c_int, c_int, _u8p, c_int, _dp, c_i64,
                                        c_double, c_i64, _dp, _dp, c_int]
         L.orc_mixture.argtypes = [c_int, c_int, c_int, _dp, _i32p, _dp, c_i64, c_int, _dp]
@@ -59,7 +63,8 @@ def lib():
         L.orc_project_gaussian.argtypes = [c_int, c_double, c_int, c_int, c_double, c_double, c_double, _dp]
         L.orc_l2_err_gaussian.argtypes = [c_int, c_double, c_int, c_int, _dp, c_double, c_double, c_double, _dp]
         for f in (L.orc_reference, L.orc_basis, L.orc_apply_L, L.orc_advance, L.orc_moments,
-                  L.orc_project_delta, L.orc_solve, L.orc_solve_points, L.orc_sigma, L.orc_project_gaussian, L.orc_l2_err_gaussian, L.orc_mixture, L.orc_residual):
+                  L.orc_project_delta, L.orc_solve, L.orc_solve_points, L.orc_sigma, L.orc_q_reference,
+                  L.orc_q_apply_L, L.orc_q_solve, L.orc_project_gaussian, L.orc_l2_err_gaussian, L.orc_mixture, L.orc_residual):
             f.restype = c_int
         _lib = L
     return _lib
@@ -160,6 +165,40 @@ def solve_points(p, h, D, mask, points, dt, nsteps, outer_bc=REFLECT, keep_densi
     dens = np.zeros((n, ny, nx, 2, ndof(p))) if keep_density else None
     _chk(lib().orc_solve_points(p, h, D, nx, ny, _p(mask, _u8p), outer_bc, _p(pts), n, dt, nsteps,
                                 _p(mom), _p(dens), nthreads), "orc_solve_points")
+    return (mom, dens) if keep_density else mom
+
+
+# ---- N4: quadrilateral Q_p elements (one per pixel), REFLECT --------------------
+def qdof(p: int) -> int:
+    return (p + 1) * (p + 1)
+
+
+def q_reference(p, h=1.0) -> dict:
+    d = qdof(p)
+    out = dict(M=np.zeros((d, d)), Minv=np.zeros((d, d)), Dc=np.zeros((2, d, d)), Em=np.zeros((4, d, d)),
+               Ep=np.zeros((4, d, d)))
+    _chk(lib().orc_q_reference(p, h, *[_p(out[k]) for k in ("M", "Minv", "Dc", "Em", "Ep")]), "orc_q_reference")
+    return out
+
+
+def q_apply_L(p, h, D, mask, u) -> np.ndarray:
+    mask = _mask(mask)
+    ny, nx = mask.shape
+    u = np.ascontiguousarray(u, dtype=np.float64).reshape(ny, nx, qdof(p))
+    out = np.zeros_like(u)
+    _chk(lib().orc_q_apply_L(p, h, D, nx, ny, _p(mask, _u8p), _p(u), _p(out)), "orc_q_apply_L")
+    return out
+
+
+def q_solve(p, h, D, mask, sources, dt, nsteps, keep_density=False, nthreads=0):
+    mask = _mask(mask)
+    ny, nx = mask.shape
+    src = np.ascontiguousarray(sources, dtype=np.int32).reshape(-1, 2)
+    n = src.shape[0]
+    mom = np.zeros((n, 6))
+    dens = np.zeros((n, ny, nx, qdof(p))) if keep_density else None
+    _chk(lib().orc_q_solve(p, h, D, nx, ny, _p(mask, _u8p), _p(src, _i32p), n, dt, nsteps, _p(mom), _p(dens),
+                           nthreads), "orc_q_solve")
     return (mom, dens) if keep_density else mom
 
 

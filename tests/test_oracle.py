@@ -510,3 +510,81 @@ def test_point_free_space_p2_closed_form_and_translation(orc):
     S, _ = orc.sigma(mom[:1])
     assert np.abs(S - 2.0 * np.eye(2)).max() <= 1e-12
     assert np.allclose(mom[0], mom[1], rtol=0, atol=1e-12)
+
+
+# ---------------------------------------------------------------- N4 quadrilateral Q_p elements
+def test_quad_q1_mass_matrix_closed_form(orc):
+    """Q1 mass matrix = (h^2/36) [[4,2,2,1],[2,4,1,2],[2,1,4,2],[1,2,2,4]] (nodes
+    (0,0),(1,0),(0,1),(1,1)); catches a wrong node order or quadrature."""
+    h = 0.6
+    R = orc.q_reference(1, h)
+    ref = h * h / 36 * np.array([[4, 2, 2, 1], [2, 4, 1, 2], [2, 1, 4, 2], [1, 2, 2, 4]])
+    assert np.allclose(R["M"], ref, rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_quad_apply_L_and_steps_match_dense(orc, p):
+    """O1's element-loop Q_p operator == O2q's dense global assembly (Vandermonde
+    basis, exact integrals) on random walled masks, and SSP-RK3 steps agree;
+    masked rows are exactly zero and 1^T M L u = 0 (no flux through walls)."""
+    from oracle import dense_quad as Q
+    rng = np.random.default_rng(70 + p)
+    d = (p + 1) ** 2
+    for _ in range(2):
+        mask = (rng.random((6, 7)) < 0.35).astype(np.uint8)
+        u = rng.standard_normal((6, 7, d))
+        u[mask.astype(bool)] = 0
+        h, D = 0.7, 1.3
+        L = Q.assemble(p, h, D, mask)
+        ref = (L @ u.reshape(-1)).reshape(u.shape)
+        got = orc.q_apply_L(p, h, D, mask, u)
+        tol = 1e-12 if p <= 2 else 1e-9          # O2q's Q3 monomial Vandermonde: cond ~1e5
+        assert np.linalg.norm(got - ref) <= tol * np.linalg.norm(ref)
+        assert np.abs(got[mask.astype(bool)]).max() == 0.0
+        M, _, _ = Q.local(p, h)
+        assert abs(np.einsum("ij,yxj->", M, got)) <= 1e-12 * np.abs(got).sum()
+    dt = 1e-3
+    steps = Q.ssprk3(L, u.reshape(-1), dt, 5).reshape(u.shape)
+    src_free = np.argwhere(mask == 0)[0][::-1]
+    mom, dens = orc.q_solve(p, h, D, mask, [tuple(src_free)], dt, 5, keep_density=True)
+    u0 = np.zeros_like(u)
+    u0[src_free[1], src_free[0]] = np.linalg.solve(Q.local(p, h)[0], _q_basis_at_centre(p))
+    assert np.allclose(dens[0], Q.ssprk3(L, u0.reshape(-1), dt, 5).reshape(u.shape), rtol=0,
+                       atol=(1e-12 if p <= 2 else 1e-9) * np.abs(dens[0]).max())
+    assert steps.shape == u.shape
+
+
+def _q_basis_at_centre(p):
+    from oracle import dense_quad as Q
+    C = Q.coeffs(p)
+    mons = [(a, b) for b in range(p + 1) for a in range(p + 1)]
+    return np.array([sum(C[m, k] * 0.5 ** (a + b) for m, (a, b) in enumerate(mons)) for k in range(len(mons))])
+
+
+def test_quad_free_space_closed_forms(orc):
+    """Free space, walls >= 48 sigma away: Q1's projected central Dirac is the
+    uniform density on the source pixel (M^-1 of N(1/2,1/2) = 1 since the Q1
+    row sums of M are 1/4), so Sigma = 2 D Delta I + (h^2/12) I; Q2 holds
+    x^2, y^2, so Sigma = 2 D Delta I exactly."""
+    m = np.zeros((96, 96), np.uint8)
+    S1, _ = orc.sigma(orc.q_solve(1, 1.0, 1.0, m, [(48, 48)], 1 / 32, 16))
+    assert np.abs(S1 - (1.0 + 1 / 12) * np.eye(2)).max() <= 1e-12
+    S2, mu2 = orc.sigma(orc.q_solve(2, 1.0, 1.0, m, [(48, 48)], 1 / 128, 64))
+    assert np.abs(S2 - 1.0 * np.eye(2)).max() <= 1e-12
+    assert np.abs(mu2).max() <= 1e-13
+
+
+def test_quad_rotation_90_and_transpose_exact(orc):
+    """Quads are D4-symmetric (no diagonal): a 90-degree rotation of a walled
+    substrate gives Sigma' = R Sigma R^T to rounding (the triangles only
+    converge in h), and the transpose swaps x and y exactly."""
+    mask, src = _case(41)
+    n = mask.shape[0]
+    S, _ = orc.sigma(orc.q_solve(2, 1.0, 1.0, mask, src, 1 / 128, 120))
+    Sr, _ = orc.sigma(orc.q_solve(2, 1.0, 1.0, np.rot90(mask).copy(), [(j, n - 1 - i) for i, j in src],
+                                  1 / 128, 120))
+    Rm = np.array([[0, -1], [1, 0]])
+    assert np.allclose(Sr, Rm @ S @ Rm.T, rtol=1e-12, atol=1e-14)
+    St, _ = orc.sigma(orc.q_solve(2, 1.0, 1.0, mask.T.copy(), [(j, i) for i, j in src], 1 / 128, 120))
+    assert np.allclose(St, S[::-1, ::-1], rtol=1e-12, atol=1e-14)
+    assert np.linalg.eigvalsh(S).min() > 0
