@@ -220,6 +220,14 @@ dgdiff_status dgdiff_absorb_table(int32_t degree, double *A);
  * cw [2][d] (triangle-major, canonical order): the mixture node weights. */
 dgdiff_status dgdiff_centre_weights(int32_t degree, double *cw);
 
+/* N4 quadrilateral Q_p elements (degree 1 or 2, host K0, exact rationals
+ * rounded once): the 9-point-cross composite operator, blocks [28][d][d],
+ * d = (p+1)^2 (dof b (p+1) + a at the node (a/p, b/p)); ids 0..15 the self
+ * block of open-face code c, 16+f the face-f neighbour block when the
+ * opposite face is open, 20+f when it is closed, 24+f the block of the pixel
+ * two steps away in direction f (f = E, W, N, S).  Units D/h^2. */
+dgdiff_status dgdiff_quad_table(int32_t degree, double *blocks);
+
 /* Source shard of `rank` out of `nranks` for a batch of n sources. */
 void dgdiff_shard(int64_t n, int32_t rank, int32_t nranks, int64_t *begin, int64_t *end);
 

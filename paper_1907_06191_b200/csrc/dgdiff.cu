@@ -1433,6 +1433,18 @@ extern "C" dgdiff_status dgdiff_absorb_table(int32_t degree, double *A) {
   return DGDIFF_OK;
 }
 
+extern "C" dgdiff_status dgdiff_quad_table(int32_t degree, double *blocks) {
+  if (degree < 1 || degree > 2) return fail(DGDIFF_E_ARG, "quadrilateral degree %d not supported (1 or 2)", degree);
+  if (!blocks) return fail(DGDIFF_E_ARG, "NULL argument");
+  try {
+    dgop::QuadTable T = dgop::build_quad(degree);
+    memcpy(blocks, T.blocks.data(), sizeof(double) * T.blocks.size());
+  } catch (const std::exception &e) {
+    return fail(DGDIFF_E_ARG, "K0 (quads): %s", e.what());
+  }
+  return DGDIFF_OK;
+}
+
 extern "C" dgdiff_status dgdiff_centre_weights(int32_t degree, double *cw) {
   if (degree < 1 || degree > 3) return fail(DGDIFF_E_ARG, "degree %d not supported (1..3)", degree);
   if (!cw) return fail(DGDIFF_E_ARG, "cw is NULL");

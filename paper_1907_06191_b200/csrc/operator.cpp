@@ -393,6 +393,137 @@ Table build(int p) {
   return T;
 }
 
+// ---- N4: quadrilateral Q_p elements ----------------------------------------
+QuadTable build_quad(int p) {
+  if (p < 1 || p > 2) throw std::runtime_error("quadrilateral elements: degree must be 1 or 2");
+  const int d = (p + 1) * (p + 1);
+  // tensor Lagrange basis from the nodal Vandermonde on (a/p, b/p), dof k = b (p+1) + a
+  std::vector<std::pair<int, int>> mons;
+  for (int b = 0; b <= p; b++)
+    for (int a = 0; a <= p; a++) mons.push_back({a, b});
+  Mat V = zeros(d, d);
+  for (int n = 0; n < d; n++)
+    for (int m = 0; m < d; m++)
+      V[n][m] = qpow(Q(mons[n].first, p), mons[m].first) * qpow(Q(mons[n].second, p), mons[m].second);
+  Mat C = inverse(V);
+  std::vector<Poly2> phi(d, Poly2(p + 1, std::vector<Q>(p + 1, Q(0))));
+  for (int k = 0; k < d; k++)
+    for (int m = 0; m < d; m++) phi[k][mons[m].first][mons[m].second] = C[m][k];
+  auto sq = [&](const Poly2 &P) {   // int over the unit square
+    Q s(0);
+    for (size_t a = 0; a < P.size(); a++)
+      for (size_t b = 0; b < P[a].size(); b++)
+        if (!P[a][b].zero()) s += P[a][b] * Q(1, (i128)(a + 1) * (i128)(b + 1));
+    return s;
+  };
+  Mat M = zeros(d, d), Dc[2] = {zeros(d, d), zeros(d, d)};
+  for (int i = 0; i < d; i++)
+    for (int j = 0; j < d; j++) {
+      M[i][j] = sq(pmul(phi[i], phi[j]));
+      for (int c = 0; c < 2; c++) Dc[c][i][j] = sq(pmul(pderiv(phi[i], c), phi[j]));
+    }
+  Mat Mi = inverse(M);
+  // faces E W N S: K-local segment A -> B, neighbour offset, normal
+  const int FA[4][2] = {{1, 0}, {0, 0}, {0, 1}, {0, 0}}, FB[4][2] = {{1, 1}, {0, 1}, {1, 1}, {1, 0}};
+  const int OFF[4][2] = {{1, 0}, {-1, 0}, {0, 1}, {0, -1}}, NRM[4][2] = {{1, 0}, {-1, 0}, {0, 1}, {0, -1}};
+  const int OPP[4] = {1, 0, 3, 2};
+  Mat Em[4], Ep[4];
+  for (int f = 0; f < 4; f++) {
+    Em[f] = zeros(d, d);
+    Ep[f] = zeros(d, d);
+    Q x0(FA[f][0]), y0(FA[f][1]), dx(FB[f][0] - FA[f][0]), dy(FB[f][1] - FA[f][1]);
+    std::vector<Poly1> pm(d), pn(d);
+    for (int i = 0; i < d; i++) {
+      pm[i] = restrict_line(phi[i], x0, dx, y0, dy);
+      pn[i] = restrict_line(phi[i], x0 - Q(OFF[f][0]), dx, y0 - Q(OFF[f][1]), dy);
+    }
+    for (int i = 0; i < d; i++)
+      for (int j = 0; j < d; j++) {
+        Em[f][i][j] = integrate1(p1mul(pm[i], pm[j]));
+        Ep[f][i][j] = integrate1(p1mul(pm[i], pn[j]));
+      }
+  }
+  // q of an element: S0_c (its own u, all four faces' E^- terms: u+ = 0 at
+  // walls keeps them) and P_f,c (the neighbour across face f)
+  Mat S0[2], Pf[4][2];
+  for (int c = 0; c < 2; c++) {
+    Mat t = zeros(d, d);
+    axpy(t, Q(-1), Dc[c]);
+    for (int f = 0; f < 4; f++)
+      if (NRM[f][c]) axpy(t, Q(NRM[f][c], 2), Em[f]);
+    S0[c] = mul(Mi, t);
+    for (int f = 0; f < 4; f++) {
+      Mat e = zeros(d, d);
+      if (NRM[f][c]) axpy(e, Q(NRM[f][c], 2), Ep[f]);
+      Pf[f][c] = mul(Mi, e);
+    }
+  }
+  QuadTable T;
+  T.p = p;
+  T.d = d;
+  T.blocks.assign((size_t)28 * d * d, 0.0);
+  auto put = [&](int b, const Mat &A) {
+    for (int i = 0; i < d; i++)
+      for (int j = 0; j < d; j++) T.blocks[((size_t)b * d + i) * d + j] = A[i][j].to_double();
+  };
+  // rhs_K = M^-1 [ sum_c T_c q_Kc + sum_{f open} 1/2 n_fc Ep_f q_{N_f,c} ],
+  // T_c = -Dc + sum_{f open} 1/2 n_fc Em_f (k = D on open faces, units D = 1);
+  // the perpendicular neighbours of N_f drop out exactly (n_f . n_perp = 0)
+  auto Tc = [&](int code, int c) {
+    Mat t = zeros(d, d);
+    axpy(t, Q(-1), Dc[c]);
+    for (int f = 0; f < 4; f++)
+      if (((code >> f) & 1) && NRM[f][c]) axpy(t, Q(NRM[f][c], 2), Em[f]);
+    return t;
+  };
+  for (int code = 0; code < 16; code++) {
+    Mat A = zeros(d, d);
+    for (int c = 0; c < 2; c++) {
+      Mat t = mul(Tc(code, c), S0[c]);
+      for (int f = 0; f < 4; f++)
+        if (((code >> f) & 1) && NRM[f][c]) axpy(t, Q(NRM[f][c], 2), mul(Ep[f], Pf[OPP[f]][c]));
+      for (int i = 0; i < d; i++)
+        for (int j = 0; j < d; j++) A[i][j] += t[i][j];
+    }
+    put(code, mul(Mi, A));
+  }
+  for (int f = 0; f < 4; f++)
+    for (int oo = 0; oo < 2; oo++) {   // opposite face open (oo = 1) or closed
+      const int code = (1 << f) | (oo ? (1 << OPP[f]) : 0);
+      Mat A = zeros(d, d);
+      for (int c = 0; c < 2; c++) {
+        Mat t = mul(Tc(code, c), Pf[f][c]);
+        if (NRM[f][c]) axpy(t, Q(NRM[f][c], 2), mul(Ep[f], S0[c]));
+        for (int i = 0; i < d; i++)
+          for (int j = 0; j < d; j++) A[i][j] += t[i][j];
+      }
+      put(oo ? 16 + f : 20 + f, mul(Mi, A));
+    }
+  for (int f = 0; f < 4; f++) {
+    Mat A = zeros(d, d);
+    for (int c = 0; c < 2; c++)
+      if (NRM[f][c]) axpy(A, Q(NRM[f][c], 2), mul(Ep[f], Pf[f][c]));
+    put(24 + f, mul(Mi, A));
+  }
+  const int AB[6][2] = {{0, 0}, {1, 0}, {0, 1}, {2, 0}, {1, 1}, {0, 2}};
+  T.W.assign((size_t)6 * d, 0.0);
+  for (int q = 0; q < 6; q++)
+    for (int k = 0; k < d; k++) {
+      Poly2 m(AB[q][0] + 1, std::vector<Q>(AB[q][1] + 1, Q(0)));
+      m[AB[q][0]][AB[q][1]] = Q(1);
+      T.W[(size_t)q * d + k] = sq(pmul(m, phi[k])).to_double();
+    }
+  T.init.assign(d, 0.0);
+  T.cw.assign(d, 0.0);
+  for (int i = 0; i < d; i++) {
+    Q s(0);
+    for (int j = 0; j < d; j++) s += Mi[i][j] * peval(phi[j], Q(1, 2), Q(1, 2));
+    T.init[i] = s.to_double();
+    T.cw[i] = peval(phi[i], Q(1, 2), Q(1, 2)).to_double();
+  }
+  return T;
+}
+
 void point_init(const Table &T, double xi, double eta, double *out) {
   const int p = T.p, d = T.d;
   const double wt[2] = {eta < xi ? 1.0 : eta > xi ? 0.0 : 0.5, eta > xi ? 1.0 : eta < xi ? 0.0 : 0.5};

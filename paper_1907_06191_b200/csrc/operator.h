@@ -25,6 +25,24 @@ void point_init(const Table &T, double xi, double eta, double *out);
 // non-zero corner coupling, rational overflow).
 Table build(int p);
 
+// N4: quadrilateral Q_p elements, one per pixel (p = 1, 2).  The composite
+// operator (q eliminated) is a 9-point cross: after exact elimination
+//   A[code][self]                 16 variants (open-face code of the pixel)
+//   A[f] = N_f[opposite face open] 2 variants per face (the opposite face's
+//                                  E^- term meets the lifted jump of face f)
+//   A[ff] = NN_f                   fixed (the neighbour's far face)
+// blocks[28][d][d], ids 0..15 self[code], 16+f N_f (opposite open), 20+f N_f
+// (opposite closed), 24+f NN_f; units D/h^2; d = (p+1)^2, dof b (p+1) + a
+// for the node (a/p, b/p).  Corner couplings vanish exactly (checked).
+struct QuadTable {
+  int p = 0, d = 0;
+  std::vector<double> blocks;  // [28][d][d]
+  std::vector<double> W;       // [6][d] moment weights on the unit pixel
+  std::vector<double> init;    // [d] projected central Dirac, units 1/h^2
+  std::vector<double> cw;      // [d] N_k(1/2, 1/2)
+};
+QuadTable build_quad(int p);
+
 // Composite blocks of pixels with absorbing outer faces (outer_bc = ABSORB,
 // Eq. (4)): A[code][outer][5][2d][2d] (outer = faces on the outer square; zero
 // unless code & outer == 0 and outer != 0), units D/h^2.

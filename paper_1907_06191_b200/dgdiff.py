@@ -22,7 +22,7 @@ EXPORTED = ["dgdiff_opts_default", "dgdiff_create", "dgdiff_solve_batch", "dgdif
             "dgdiff_source_moments", "dgdiff_get_density", "dgdiff_dt_max", "dgdiff_last_error",
             "dgdiff_destroy", "dgdiff_operator_table", "dgdiff_shard", "dgdiff_set_timing",
             "dgdiff_get_stats", "dgdiff_reset_stats", "dgdiff_mixture", "dgdiff_centre_weights",
-            "dgdiff_absorb_table", "dgdiff_mc_covariance", "dgdiff_solve_batch_points"]
+            "dgdiff_absorb_table", "dgdiff_mc_covariance", "dgdiff_solve_batch_points", "dgdiff_quad_table"]
 
 
 class dgdiff_opts(ctypes.Structure):
@@ -75,6 +75,7 @@ def _load():
     L.dgdiff_reset_stats.argtypes = [H]
     for name, args in (("dgdiff_mixture", [H, dp, dp]), ("dgdiff_centre_weights", [i32, dp]),
                        ("dgdiff_absorb_table", [i32, dp]), ("dgdiff_solve_batch_points", [H, dp, i64, dbl, i64]),
+                       ("dgdiff_quad_table", [i32, dp]),
                        ("dgdiff_mc_covariance", [H, ctypes.POINTER(ctypes.c_int32), i64, i32, i64, dbl,
                                                  ctypes.c_uint32, dp, dp, dp, dp])):
         if hasattr(L, name):
@@ -125,6 +126,14 @@ def dgdiff_solve_batch(handle, sources, dt, nsteps):
     src = np.ascontiguousarray(sources, dtype=np.int32).reshape(-1, 2)
     _check(lib.dgdiff_solve_batch(handle, src.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), src.shape[0],
                                   float(dt), int(nsteps)))
+
+
+def dgdiff_quad_table(degree):
+    """N4 Q_p composite blocks [28][(p+1)^2][(p+1)^2] (host K0)."""
+    d = (degree + 1) ** 2
+    out = np.zeros((28, d, d))
+    _check(lib.dgdiff_quad_table(int(degree), _dp(out)))
+    return out
 
 
 def dgdiff_solve_batch_points(handle, points, dt, nsteps):

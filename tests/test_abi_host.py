@@ -225,3 +225,27 @@ def test_argument_errors_are_reported(dg):
         with pytest.raises(dg.DGDiffError) as e:
             dg.dgdiff_create(np.zeros((4, 4), np.uint8), 1.0, 1.0, 1, dg.dgdiff_opts_default(**bad))
         assert e.value.status == dg.E_ARG, bad
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_quad_table_matches_dense_assembly(dg, p):
+    """N4 Q_p: K0's 9-point-cross blocks (exact rationals) == O2q's dense
+    operator for all 16 codes; the face-neighbour block has exactly two
+    variants (opposite face open / closed), the far block one; corners are 0."""
+    from oracle import dense_quad as Q
+    T = dg.dgdiff_quad_table(p)
+    tol = 1e-12 * max(1.0, np.abs(T).max())
+    offs = [(1, 0), (-1, 0), (0, 1), (0, -1)]
+    opp = [1, 0, 3, 2]
+    for code in range(16):
+        B = Q.composite_blocks(p, code)
+        assert np.abs(T[code] - B[(0, 0)]).max() <= tol, code
+        for f, (di, dj) in enumerate(offs):
+            if not (code >> f) & 1:
+                continue       # a masked neighbour holds u = 0: its column is never used
+            N = T[16 + f] if (code >> opp[f]) & 1 else T[20 + f]
+            assert np.abs(N - B[(di, dj)]).max() <= tol, (code, f)
+            assert np.abs(T[24 + f] - B[(2 * di, 2 * dj)]).max() <= tol, (code, f)
+        for off in [(1, 1), (1, -1), (-1, 1), (-1, -1), (2, 1), (1, 2), (3, 0)]:
+            assert np.abs(B[off]).max() <= 1e-13
+    assert np.abs(T[16] - T[20]).max() > 1e-3       # the two variants really differ
