@@ -95,6 +95,13 @@ typedef struct {
                              rounding; moments are returned in input order).
                              Ring kernel only (kernel 1/2, temporal_steps 2 ->
                              E_ARG).  0 (default) = whole grid */
+  int32_t element;        /* 0 (default) = two P_p triangles per pixel;
+                             1 = one Q_p quadrilateral per pixel (N4, the north
+                             star's "Q2"; degree 1 or 2): tensor Lagrange basis
+                             on (a/p, b/p), dof b (p+1) + a, same fluxes; the
+                             composite operator is a 9-point cross.  Default
+                             ring kernel and REFLECT only; densities are
+                             [ny][nx][(p+1)^2] */
 } dgdiff_opts;
 
 /* Fill *o with the defaults above. */

@@ -134,7 +134,8 @@ __global__ void __launch_bounds__(256) k_moments(const T *__restrict__ U, const 
                                                  const double2 *__restrict__ src_xy, int nact, int ngroups,
                                                  int px_per_cta, double *__restrict__ partial,
                                                  int64_t chunk, const int2 *__restrict__ grange /* nullable (N1) */) {
-  constexpr int G = 32 * NV, d = D2 / 2;
+  constexpr int NT = (D2 == 4 || D2 == 9) ? 1 : 2;   // elements per pixel (quads: 1)
+  constexpr int G = 32 * NV, d = D2 / NT;
   const int lane = threadIdx.x & 31;
   const int g = blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (g >= ngroups) return;
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(256) k_moments(const T *__restrict__ U, const 
     for (int e = 0; e < NV; e++) {
       double P[6] = {0, 0, 0, 0, 0, 0};
 #pragma unroll
-      for (int t = 0; t < 2; t++)
+      for (int t = 0; t < NT; t++)
 #pragma unroll
         for (int q = 0; q < 6; q++)
 #pragma unroll
@@ -296,7 +297,8 @@ template <typename T, int NV, int D2>
 __global__ void k_mixture(const T *__restrict__ U, const int *__restrict__ aidx, int nx, int ny, int nact,
                           const int2 *__restrict__ src_ij, const double *__restrict__ mom, int64_t nvalid, int R,
                           double *__restrict__ grid, const int2 *__restrict__ grange /* nullable (N1) */) {
-  constexpr int G = 32 * NV, d = D2 / 2;
+  constexpr int NT = (D2 == 4 || D2 == 9) ? 1 : 2;
+  constexpr int G = 32 * NV, d = D2 / NT;
   const int side = 2 * R + 1;
   const int cell = blockIdx.x * blockDim.x + threadIdx.x;
   if (cell >= side * side) return;
@@ -319,9 +321,9 @@ __global__ void k_mixture(const T *__restrict__ U, const int *__restrict__ aidx,
 #pragma unroll
     for (int k = 0; k < d; k++) {
       vl += c_CW[k] * (double)p[(size_t)k * G];
-      vu += c_CW[DMAXK + k] * (double)p[(size_t)(d + k) * G];
+      if (NT == 2) vu += c_CW[DMAXK + k] * (double)p[(size_t)(d + k) * G];
     }
-    acc += 0.5 * (vl + vu) / mom[s * 6];
+    acc += (NT == 2 ? 0.5 * (vl + vu) : vl) / mom[s * 6];   // quads: one element, its centre value
   }
   grid[cell] += acc;
 }
@@ -425,6 +427,8 @@ struct dgdiff_s {
   double *d_out = nullptr;
   // N1 active windows
   bool windows = false;
+  bool quad = false;                               // N4 quadrilateral Q_p elements (opts.element = 1)
+  int halo = 1;                                    // composite stencil reach (quads: 2)
   int32_t *d_srcw = nullptr, *d_perm = nullptr;   // sorted local sources [nloc][2], their global indices
   int64_t srcw_cap = 0;
   double *d_momc = nullptr;                        // chunk-ordered moment rows (sorted order)
@@ -480,6 +484,7 @@ static int lane_nv(const dgdiff_s *H) {
   const int ts = (int)tsize(H);
   if (H->o.kernel == 1 || H->o.kernel == 2) return 16 / ts;
   if (use_fused(H)) return 1;
+  if (H->quad) return 8 / ts;
   return (H->p == 1 ? 16 : 8) / ts;
 }
 static int gsize(const dgdiff_s *H) { return 32 * lane_nv(H); }
@@ -606,14 +611,35 @@ static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
     H->own_stream = true;
   }
   // K0 operator tables
+  dgop::QuadTable qt;
   try {
-    H->tab = dgop::build(H->p);
+    if (H->quad) qt = dgop::build_quad(H->p);
+    else H->tab = dgop::build(H->p);
   } catch (std::exception &ex) {
     return fail(DGDIFF_E_ARG, "operator precompute failed: %s", ex.what());
   }
+  if (H->quad) {
+    // compiled Q tables == this run's K0; moment weights / init / centre values
+    // in the triangle layout with t = 0 only
+    const int d = H->D2;
+    for (int b = 0; b < 28; b++)
+      for (int r = 0; r < d; r++)
+        for (int c = 0; c < d; c++) {
+          const double v = H->p == 1 ? dgk::tab<101>(b, r, c) : dgk::tab<102>(b, r, c);
+          if (v != qt.blocks[((size_t)b * d + r) * d + c]) return fail(DGDIFF_E_ARG, "compiled Q table differs from K0");
+        }
+    H->tab.p = H->p;
+    H->tab.d = d;
+    H->tab.W.assign((size_t)2 * 6 * d, 0.0);
+    for (int q = 0; q < 6; q++)
+      for (int k = 0; k < d; k++) H->tab.W[(size_t)q * d + k] = qt.W[(size_t)q * d + k];
+    H->tab.init = qt.init;
+    H->tab.cw.assign((size_t)2 * d, 0.0);
+    for (int k = 0; k < d; k++) H->tab.cw[k] = qt.cw[k];
+  }
   // the kernels carry the operator as compile-time immediates (tables.inc,
   // generated from K0 at build time): check them against this run's K0
-  {
+  if (!H->quad) {
     const int D2 = H->D2;
     auto A = [&](int code, int o, int r, int c) { return H->tab.A[(((size_t)code * 5 + o) * D2 + r) * D2 + c]; };
     for (int code = 0; code < 16; code++)
@@ -657,6 +683,16 @@ static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
     int i = pix[a].x, j = pix[a].y;
     nbr[a] = make_int4(at(i + 1, j), at(i - 1, j), at(i, j + 1), at(i, j - 1));
   }
+  // quads: [a][2] int4 = E W N S, then the pixels two steps away EE WW NN SS
+  std::vector<int4> nbr_q;
+  if (H->quad) {
+    nbr_q.resize((size_t)2 * H->nact);
+    for (int64_t a = 0; a < H->nact; a++) {
+      int i = pix[a].x, j = pix[a].y;
+      nbr_q[2 * a] = nbr[a];
+      nbr_q[2 * a + 1] = make_int4(at(i + 2, j), at(i - 2, j), at(i, j + 2), at(i, j - 2));
+    }
+  }
   // ring kernel row tables (one per strip width: the stage without the alpha
   // term may use wider strips): active-index bounds of every (strip, row) tile
   if (use_ring(H)) {
@@ -671,14 +707,15 @@ static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
     }
     for (int va = 0; va < 2; va++) {
       const bool alpha = va == 1;
-      const int W = dgl::ring_width(H->p, alpha);
+      const int W = dgl::ring_width(H->quad ? 100 + H->p : H->p, alpha);
       const int ns = (nx + W - 1) / W;
+      const int hl = H->halo;
       std::vector<int4> rtab((size_t)ns * ny);
       for (int s = 0; s < ns; s++)
         for (int j = 0; j < ny; j++) {
           const int x0 = s * W;
           auto c = [&](int x) { return cum[(size_t)j * (nx + 1) + std::max(0, std::min(nx, x))]; };
-          rtab[(size_t)s * ny + j] = make_int4(c(x0 - 1), c(x0), c(x0 + W), c(x0 + W + 1));
+          rtab[(size_t)s * ny + j] = make_int4(c(x0 - hl), c(x0), c(x0 + W), c(x0 + W + hl));
         }
       // mean halo.d row-tile size (pixel tiles): the ring kernel without the
       // alpha term keeps ~8 mean rows in flight (measured optimum on c2/c4:
@@ -701,7 +738,7 @@ static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
   }
   // fused-step row table (P1): bounds of the u (3-column halo), U1 (2), U2 (1)
   // and output ranges of every (strip, row)
-  if (H->p == 1) {
+  if (H->p == 1 && !H->quad) {
     const int W = dgl::fused_width(H->o.precision);
     H->nstrips3 = (nx + W - 1) / W;
     std::vector<int> cum((size_t)ny * (nx + 1));
@@ -725,10 +762,11 @@ static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
     CK(cudaMemcpy(H->d_rowtab3, rt3.data(), sizeof(int4) * rt3.size(), cudaMemcpyHostToDevice));
   }
   H->nsm = prop.multiProcessorCount;
-  CK(cudaMalloc(&H->d_nbr, sizeof(int4) * H->nact));
+  const std::vector<int4> &nbr_dev = H->quad ? nbr_q : nbr;
+  CK(cudaMalloc(&H->d_nbr, sizeof(int4) * nbr_dev.size()));
   CK(cudaMalloc(&H->d_pix, sizeof(int2) * H->nact));
   CK(cudaMalloc(&H->d_aidx, sizeof(int) * (size_t)nx * ny));
-  CK(cudaMemcpy(H->d_nbr, nbr.data(), sizeof(int4) * H->nact, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(H->d_nbr, nbr_dev.data(), sizeof(int4) * nbr_dev.size(), cudaMemcpyHostToDevice));
   // algorithmic MACs of one stage (per source): structural non-zeros of the
   // pixel's self block plus its open neighbour blocks
   {
@@ -736,6 +774,20 @@ static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
     for (int64_t a = 0; a < H->nact; a++) {
       const int4 nb = nbr[a];
       const int code = (nb.x >= 0) | ((nb.y >= 0) << 1) | ((nb.z >= 0) << 2) | ((nb.w >= 0) << 3);
+      if (H->quad) {
+        const int d = H->D2, opp[4] = {1, 0, 3, 2};
+        auto nnz = [&](int b) {
+          int k = 0;
+          for (int e = 0; e < d * d; e++) k += qt.blocks[(size_t)b * d * d + e] != 0.0;
+          return k;
+        };
+        const int4 n2 = nbr_q[2 * a + 1];
+        const int far[4] = {n2.x, n2.y, n2.z, n2.w};
+        macs += nnz(code);
+        for (int f = 0; f < 4; f++)
+          if ((code >> f) & 1) macs += nnz(((code >> opp[f]) & 1) ? 16 + f : 20 + f) + (far[f] >= 0 ? nnz(24 + f) : 0);
+        continue;
+      }
       macs += H->tab.nnz[code * 5 + 0];
       for (int f = 0; f < 4; f++)
         if ((code >> f) & 1) macs += H->tab.nnz[code * 5 + 1 + f];
@@ -746,7 +798,9 @@ static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
   CK(cudaMemcpy(H->d_aidx, aidx.data(), sizeof(int) * (size_t)nx * ny, cudaMemcpyHostToDevice));
   // operator table in the state precision (exact: dyadic entries)
   size_t na = H->tab.A.size();
-  if (H->o.precision == 32) {
+  if (na == 0) {
+    // quads: the v1 table kernel does not exist for them
+  } else if (H->o.precision == 32) {
     std::vector<float> A32(na);
     for (size_t k = 0; k < na; k++) A32[k] = (float)H->tab.A[k];
     CK(cudaMalloc(&H->d_A, na * sizeof(float)));
@@ -775,6 +829,7 @@ static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
   for (int t = 0; t < 2; t++)
     for (int q = 0; q < 6; q++)
       for (int j = 0; j < H->d; j++) W[(t * 6 + q) * DMAXK + j] = H->tab.W[(t * 6 + q) * H->d + j];
+  // (quads: H->d = D2, t = 1 rows are zero and unused)
   CK(cudaMemcpyToSymbol(c_W, W, sizeof W));
   double CWv[2 * DMAXK] = {0};
   for (int t = 0; t < 2; t++)
@@ -838,6 +893,9 @@ extern "C" dgdiff_status dgdiff_create(dgdiff_t *out, const uint8_t *mask, int32
   if (o.windows == 1 && (o.kernel == 1 || o.kernel == 2 || o.temporal_steps == 2))
     return fail(DGDIFF_E_ARG, "windows (N1) run on the default ring kernel only");
   if (o.centering != 0 && o.centering != 1) return fail(DGDIFF_E_ARG, "centering must be 0 or 1");
+  if (o.element != 0 && o.element != 1) return fail(DGDIFF_E_ARG, "element must be 0 (triangles) or 1 (quadrilaterals)");
+  if (o.element == 1 && (degree > 2 || o.kernel == 1 || o.kernel == 2 || o.temporal_steps == 2 || o.outer_bc != 0))
+    return fail(DGDIFF_E_ARG, "quadrilateral Q_p (N4): degree 1 or 2, default ring kernel, REFLECT only");
   if (o.nranks < 1 || o.rank < 0 || o.rank >= o.nranks) return fail(DGDIFF_E_ARG, "bad rank/nranks");
   if (o.temporal_steps < 0) return fail(DGDIFF_E_ARG, "temporal_steps < 0");
   if (o.max_chunk < 0) return fail(DGDIFF_E_ARG, "max_chunk < 0");
@@ -846,6 +904,12 @@ extern "C" dgdiff_status dgdiff_create(dgdiff_t *out, const uint8_t *mask, int32
   H->nx = nx; H->ny = ny; H->h = h; H->D = D; H->p = degree;
   H->d = (degree + 1) * (degree + 2) / 2;
   H->D2 = 2 * H->d;
+  if (o.element == 1) {   // one Q_p element per pixel
+    H->quad = true;
+    H->halo = 2;
+    H->D2 = (degree + 1) * (degree + 1);
+    H->d = H->D2;
+  }
   H->o = o;
   memset(&H->st, 0, sizeof H->st);
   dgdiff_status s = create_impl(H, mask);
@@ -920,7 +984,7 @@ static dgdiff_status run_chunk(dgdiff_s *H, int64_t nvalid, int64_t chunk, doubl
     if (!begin) H->sev_pending[k] = true;
     return DGDIFF_OK;
   };
-  constexpr int P = D2 == 6 ? 1 : D2 == 12 ? 2 : 3;
+  constexpr int P = D2 == 6 ? 1 : D2 == 12 ? 2 : D2 == 20 ? 3 : D2 == 4 ? 101 : 102;
   dgl::StageArgs sa;
   sa.nbr = H->d_nbr;
   sa.A = A;
@@ -964,7 +1028,7 @@ static dgdiff_status run_chunk(dgdiff_s *H, int64_t nvalid, int64_t chunk, doubl
     sa.alpha = alpha;
     sa.cs = cs;
     if (H->windows) {
-      sa.wr = (int)std::min<int64_t>(1 << 30, 3 * cur_step + k + 1);   // output support radius
+      sa.wr = (int)std::min<int64_t>(1 << 30, H->halo * (3 * cur_step + k + 1));   // output support radius
       double px = 0;
       for (int g = 0; g < ngroups; g++) px += box_px(g, sa.wr);
       win_bytes += (k == 0 ? 2.0 : 3.0) * px * D2 * G * sizeof(T);
@@ -1058,11 +1122,15 @@ static dgdiff_status run_chunk_p(dgdiff_s *H, int64_t nvalid, int64_t chunk, dou
   if (nv == 1) {
     if (H->D2 == 6) return run_chunk<T, 1, 6>(H, nvalid, chunk, dt, nsteps, mom_rows);
     if (H->D2 == 20) return run_chunk<T, 1, 20>(H, nvalid, chunk, dt, nsteps, mom_rows);
+    if (H->D2 == 4) return run_chunk<T, 1, 4>(H, nvalid, chunk, dt, nsteps, mom_rows);
+    if (H->D2 == 9) return run_chunk<T, 1, 9>(H, nvalid, chunk, dt, nsteps, mom_rows);
     return run_chunk<T, 1, 12>(H, nvalid, chunk, dt, nsteps, mom_rows);
   }
   if (nv == 2) {
     if (H->D2 == 6) return run_chunk<T, 2, 6>(H, nvalid, chunk, dt, nsteps, mom_rows);
     if (H->D2 == 20) return run_chunk<T, 2, 20>(H, nvalid, chunk, dt, nsteps, mom_rows);
+    if (H->D2 == 4) return run_chunk<T, 2, 4>(H, nvalid, chunk, dt, nsteps, mom_rows);
+    if (H->D2 == 9) return run_chunk<T, 2, 9>(H, nvalid, chunk, dt, nsteps, mom_rows);
     return run_chunk<T, 2, 12>(H, nvalid, chunk, dt, nsteps, mom_rows);
   }
   if constexpr (sizeof(T) == 4) {
@@ -1080,7 +1148,10 @@ static dgdiff_status solve_impl(dgdiff_s *H, const int32_t *sources, const doubl
   if (n < 1 || !sources) return fail(DGDIFF_E_ARG, "need n >= 1 sources");
   if (n >= (1LL << 31)) return fail(DGDIFF_E_ARG, "too many sources");
   if (nsteps < 0 || !(dt > 0) || !std::isfinite(dt)) return fail(DGDIFF_E_ARG, "need dt > 0, nsteps >= 0");
-  double dtmax = dgdiff_dt_max(H->p, H->h, H->D);
+  // quads: Bloch spectral radius of the 9-point-cross operator (N4; DESIGN
+  // reading R22): rho_Q1 = 32, rho_Q2 = 130.7
+  double dtmax = H->quad ? 2.5127453 / (H->p == 1 ? 32.0 : 130.7) * H->h * H->h / H->D
+                         : dgdiff_dt_max(H->p, H->h, H->D);
   if (dt > dtmax)
     return fail(DGDIFF_E_UNSTABLE, "dt = %.17g exceeds the SSP-RK3 limit %.17g for P%d", dt, dtmax, H->p);
   for (int64_t s = 0; s < n; s++) {
@@ -1230,7 +1301,7 @@ static dgdiff_status solve_impl(dgdiff_s *H, const int32_t *sources, const doubl
         // maintained active range per group: whole rows the group's stages can
         // read, [y0 - R - 1, y1 + R + 1] with R = 3 nsteps (raster order: contiguous)
         std::vector<int2> rng(ng);
-        const int64_t R = std::min<int64_t>(3 * nsteps + 1, H->ny);
+        const int64_t R = std::min<int64_t>(H->halo * (3 * nsteps + 1), H->ny);
         for (int64_t g = 0; g < ng; g++) {
           const int y0 = (int)std::max<int64_t>(0, H->h_gbox[g].z - R);
           const int y1 = (int)std::min<int64_t>(H->ny, H->h_gbox[g].w + R + 1);
@@ -1281,6 +1352,7 @@ extern "C" dgdiff_status dgdiff_solve_batch_points(dgdiff_t H, const double *poi
                                                    int64_t nsteps) {
   if (!H) return fail(DGDIFF_E_ARG, "handle is NULL");
   if (n < 1 || !points) return fail(DGDIFF_E_ARG, "need n >= 1 points");
+  if (H->quad) return fail(DGDIFF_E_ARG, "sub-pixel points are implemented for the triangle elements only");
   if (n >= (1LL << 31)) return fail(DGDIFF_E_ARG, "too many sources");
   const int PXS = 2 + H->D2;
   std::vector<int32_t> pix((size_t)2 * n);
@@ -1489,6 +1561,8 @@ extern "C" dgdiff_status dgdiff_get_density(dgdiff_t H, int64_t src, double *out
 #define DG_GATHER(TT, NVV)                                                                                     \
   if (H->D2 == 6) k_gather<TT, NVV, 6><<<blocks, 256, 0, H->stream>>>((TT *)H->d_U[0], (int)H->nact, g, slot, d_tmp); \
   else if (H->D2 == 20) k_gather<TT, NVV, 20><<<blocks, 256, 0, H->stream>>>((TT *)H->d_U[0], (int)H->nact, g, slot, d_tmp); \
+  else if (H->D2 == 4) k_gather<TT, NVV, 4><<<blocks, 256, 0, H->stream>>>((TT *)H->d_U[0], (int)H->nact, g, slot, d_tmp); \
+  else if (H->D2 == 9) k_gather<TT, NVV, 9><<<blocks, 256, 0, H->stream>>>((TT *)H->d_U[0], (int)H->nact, g, slot, d_tmp); \
   else k_gather<TT, NVV, 12><<<blocks, 256, 0, H->stream>>>((TT *)H->d_U[0], (int)H->nact, g, slot, d_tmp);
   if (H->o.precision == 32) {
     if (nv == 1) { DG_GATHER(float, 1) } else if (nv == 2) { DG_GATHER(float, 2) } else { DG_GATHER(float, 4) }

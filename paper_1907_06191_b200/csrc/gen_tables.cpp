@@ -84,12 +84,33 @@ static int emit(FILE *f, int p) {
   return 0;
 }
 
+// N4 quads: 28 blocks of (p+1)^2 (0..15 self[code], 16+f N_f opposite open,
+// 20+f N_f opposite closed, 24+f NN_f), as tab_q<p>(b, r, c)
+static int emit_quad(FILE *f, int p) {
+  dgop::QuadTable T = dgop::build_quad(p);
+  const int d = T.d;
+  fprintf(f, "// Q%d: 28 blocks of %dx%d (0-15 self[code], 16+f N_f opp. open, 20+f N_f opp. closed, 24+f NN_f)\n", p, d, d);
+  fprintf(f, "__host__ __device__ constexpr double tab_q%d(int b, int r, int c) {\n  switch ((b * %d + r) * %d + c) {\n", p, d, d);
+  int nnz = 0;
+  for (int b = 0; b < 28; b++)
+    for (int r = 0; r < d; r++)
+      for (int c = 0; c < d; c++) {
+        const double v = T.blocks[((size_t)b * d + r) * d + c];
+        if (v != 0.0) {
+          fprintf(f, "    case %d: return %a;\n", (b * d + r) * d + c, v);
+          nnz++;
+        }
+      }
+  fprintf(f, "    default: return 0.0;\n  }\n}\n// nnz(Q%d) = %d\n\n", p, nnz);
+  return 0;
+}
+
 int main(int argc, char **argv) {
   if (argc < 2) { fprintf(stderr, "usage: gen_tables out.inc\n"); return 2; }
   FILE *f = fopen(argv[1], "w");
   if (!f) return 2;
   fprintf(f, "// tables.inc -- GENERATED at build time by gen_tables (K0, operator.cpp). Do not edit.\n#pragma once\n\n");
-  int rc = emit(f, 1) || emit(f, 2) || emit(f, 3);
+  int rc = emit(f, 1) || emit(f, 2) || emit(f, 3) || emit_quad(f, 1) || emit_quad(f, 2);
   fclose(f);
   return rc;
 }

@@ -12,6 +12,14 @@ int ring_width(int P, bool alpha) {
     return m == RING_PLAIN ? RingCfg<1, 16, RING_PLAIN>::W
            : m == RING_U0_STAGED ? RingCfg<1, 16, RING_U0_STAGED>::W : RingCfg<1, 16, RING_U0_DIRECT>::W;
   }
+  if (P == 101 || P == 102) {
+    const int m1 = ring_mode<101>(alpha), m2 = ring_mode<102>(alpha);
+    if (P == 101)
+      return m1 == RING_PLAIN ? RingCfg<101, 8, RING_PLAIN>::W
+             : m1 == RING_U0_STAGED ? RingCfg<101, 8, RING_U0_STAGED>::W : RingCfg<101, 8, RING_U0_DIRECT>::W;
+    return m2 == RING_PLAIN ? RingCfg<102, 8, RING_PLAIN>::W
+           : m2 == RING_U0_STAGED ? RingCfg<102, 8, RING_U0_STAGED>::W : RingCfg<102, 8, RING_U0_DIRECT>::W;
+  }
   if (P == 3) {
     const int m = ring_mode<3>(alpha);
     return m == RING_PLAIN ? RingCfg<3, 8, RING_PLAIN>::W
@@ -27,6 +35,7 @@ cudaError_t launch_stage(int which, int prec, int P, bool alpha, const StageArgs
     return prec == 64 ? launch_v12_f64(which, P, alpha, a) : launch_v12_f32(which, P, alpha, a);
   if (P == 1) return prec == 64 ? launch_ring_p1_f64(alpha, a) : launch_ring_p1_f32(alpha, a);
   if (P == 3) return prec == 64 ? launch_ring_p3_f64(alpha, a) : launch_ring_p3_f32(alpha, a);
+  if (P > 100) return prec == 64 ? launch_ring_q_f64(P, alpha, a) : launch_ring_q_f32(P, alpha, a);
   return prec == 64 ? launch_ring_p2_f64(alpha, a) : launch_ring_p2_f32(alpha, a);
 }
 

@@ -32,7 +32,8 @@ struct StageArgs {
 
 // which: 0 = v1 (table in gmem), 1 = v2 (immediates), 2 = v3 ring (bulk TMA)
 cudaError_t launch_stage(int which, int prec, int P, bool alpha, const StageArgs &a);
-// strip width of the ring kernel for degree P (its row table depends on it)
+// strip width of the ring kernel for degree code P (1..3 triangles, 101/102
+// quads; its row table depends on it)
 int ring_width(int P, bool alpha);
 // K3: one fused SSP-RK3 step per pass (P1); a.rowtab = rowtab3 [nstrips][ny][2]
 cudaError_t launch_step_fused(int prec, const StageArgs &a);
@@ -49,5 +50,7 @@ cudaError_t launch_ring_p2_f64(bool alpha, const StageArgs &a);
 cudaError_t launch_ring_p2_f32(bool alpha, const StageArgs &a);
 cudaError_t launch_ring_p3_f64(bool alpha, const StageArgs &a);
 cudaError_t launch_ring_p3_f32(bool alpha, const StageArgs &a);
+cudaError_t launch_ring_q_f64(int P, bool alpha, const StageArgs &a);   // P = 101 (Q1), 102 (Q2)
+cudaError_t launch_ring_q_f32(int P, bool alpha, const StageArgs &a);
 
 }  // namespace dgl

@@ -71,6 +71,15 @@ template <> struct RingCfg<2, 8, RING_U0_DIRECT> { static constexpr int W = 16, 
 template <> struct RingCfg<3, 8, RING_PLAIN> { static constexpr int W = 8, NC = 8; };
 template <> struct RingCfg<3, 8, RING_U0_STAGED> { static constexpr int W = 8, NC = 8; };
 template <> struct RingCfg<3, 8, RING_U0_DIRECT> { static constexpr int W = 8, NC = 8; };
+// N4 quadrilaterals: degree codes 101 (Q1), 102 (Q2); their composite
+// operator is a 9-point cross, so strips carry a 2-column halo, a pixel of
+// row j reads rows j-2..j+2 and each pixel has 8 neighbour indices
+template <> struct RingCfg<101, 8, RING_PLAIN> { static constexpr int W = 16, NC = 8; };
+template <> struct RingCfg<101, 8, RING_U0_STAGED> { static constexpr int W = 16, NC = 8; };
+template <> struct RingCfg<101, 8, RING_U0_DIRECT> { static constexpr int W = 16, NC = 8; };
+template <> struct RingCfg<102, 8, RING_PLAIN> { static constexpr int W = 8, NC = 8; };
+template <> struct RingCfg<102, 8, RING_U0_STAGED> { static constexpr int W = 8, NC = 8; };
+template <> struct RingCfg<102, 8, RING_U0_DIRECT> { static constexpr int W = 8, NC = 8; };
 template <int P> constexpr int ring_mode(bool alpha) {
   return alpha ? (ring_u0_direct<P>() ? RING_U0_DIRECT : RING_U0_STAGED) : RING_PLAIN;
 }
@@ -78,7 +87,9 @@ template <int P> constexpr int ring_mode(bool alpha) {
 template <typename T, int NV, int P, bool ALPHA>
 struct RingGeom {
   static constexpr int G = 32 * NV;
-  static constexpr int D2 = (P + 1) * (P + 2);
+  static constexpr int D2 = ndof_px<P>();
+  static constexpr int HALO = halo_of<P>();                     // strip / band halo (quads: 2)
+  static constexpr int NBW = HALO;                               // int4 neighbour entries per pixel
   static constexpr bool R2U = ALPHA && !ring_u0_direct<P>();   // u0 tiles staged in ring 2
   static constexpr int W = RingCfg<P, NV * (int)sizeof(T), ring_mode<P>(ALPHA)>::W;
   static constexpr int NC = RingCfg<P, NV * (int)sizeof(T), ring_mode<P>(ALPHA)>::NC;
@@ -88,16 +99,17 @@ struct RingGeom {
   // ring 2 holds staged u0 tiles (R2U) and neighbour indices; otherwise it
   // only holds the 16-byte indices and ring 1 takes the rest
   static constexpr int N2 = R2U ? 4 * W : 16 * W;
-  static constexpr int N1 = R2U ? 4 * (W + 2) : RING_N1_NOALPHA(W, PXB, SMEM_MAX - EXTRA - N2 * 16);
+  static constexpr int ROWS_MIN = 2 * HALO + 2;                 // rows held + 1 in flight
+  static constexpr int N1 = R2U ? ROWS_MIN * (W + 2 * HALO) : RING_N1_NOALPHA(W, PXB, SMEM_MAX - EXTRA - N2 * 16 * NBW);
   static constexpr int OFF_R2 = N1 * PXB;
   static constexpr int OFF_NB = OFF_R2 + (R2U ? N2 * PXB : 0);
-  static constexpr int OFF_BAR = OFF_NB + N2 * 16;
+  static constexpr int OFF_BAR = OFF_NB + N2 * 16 * NBW;
   static constexpr int OFF_META = OFF_BAR + 2 * RING_Q * 8;
   static constexpr int OFF_RT = OFF_META + RING_Q * 32;
   static constexpr int SMEM = OFF_RT + (RING_MAXBAND + 2) * 16 + 2 * RING_Q * 4;
   static constexpr int THREADS = (NC + 1) * 32;
   static_assert(SMEM <= SMEM_MAX, "ring does not fit in shared memory");
-  static_assert(N1 >= 4 * (W + 2) && N2 >= 4 * W, "rings too small for progress");
+  static_assert(N1 >= ROWS_MIN * (W + 2 * HALO) && N2 >= ROWS_MIN * W, "rings too small for progress");
 };
 
 // Work item -> (strip s, group g, computed rows [jb0, jb1)); false if the item
@@ -170,7 +182,7 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
     for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
       int s, g, jb0, jb1;
       if (!ring_item<Gm::W>(item, nstrips, ngroups, band_rows, ny, gbox, wr, s, g, jb0, jb1)) continue;
-      const int lo = max(0, jb0 - 1), hi = min(ny - 1, jb1);
+      const int lo = max(0, jb0 - Gm::HALO), hi = min(ny - 1, jb1 - 1 + Gm::HALO);
       __syncwarp();
       for (int r = lo + lane; r <= hi; r += 32) rt[r - lo] = __ldg(&rowtab[(size_t)s * ny + r]);
       __syncwarp();
@@ -219,7 +231,7 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
           meta[q] = m;
           rv[q] = v1 + e1;
           rv[Q + q] = v2 + e2;
-          const uint32_t bytes = n1 * PXB + (Gm::R2U ? n2 * PXB : 0u) + n2 * 16u;
+          const uint32_t bytes = n1 * PXB + (Gm::R2U ? n2 * PXB : 0u) + n2 * 16u * Gm::NBW;
           mbar_expect_tx(&full[q], bytes);
           if (n1) {
             const uint32_t a1 = min(n1, (uint32_t)Gm::N1 - p1);
@@ -234,8 +246,9 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
               bulk_g2s(ring2 + (size_t)p2 * PXB, src, a2 * PXB, &full[q]);
               if (n2 > a2) bulk_g2s(ring2, src + (size_t)a2 * D2 * G, (n2 - a2) * PXB, &full[q]);
             }
-            bulk_g2s(nbr_ring + p2, nbr + t.y, a2 * 16u, &full[q]);
-            if (n2 > a2) bulk_g2s(nbr_ring, nbr + t.y + a2, (n2 - a2) * 16u, &full[q]);
+            bulk_g2s(nbr_ring + (size_t)p2 * Gm::NBW, nbr + (size_t)t.y * Gm::NBW, a2 * 16u * Gm::NBW, &full[q]);
+            if (n2 > a2)
+              bulk_g2s(nbr_ring, nbr + ((size_t)t.y + a2) * Gm::NBW, (n2 - a2) * 16u * Gm::NBW, &full[q]);
           }
         }
         // advance by the issued prefix
@@ -258,7 +271,7 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
     int s_, g, jb0, jb1;
     if (!ring_item<Gm::W>(item, nstrips, ngroups, band_rows, ny, gbox, wr, s_, g, jb0, jb1)) continue;
-    const int lo = max(0, jb0 - 1), hi = min(ny - 1, jb1);
+    const int lo = max(0, jb0 - Gm::HALO), hi = min(ny - 1, jb1 - 1 + Gm::HALO);
     T *Uog = Uout + g * gstride + lane * NV;
     const T *U0l = U0 + g * gstride + lane * NV;
     auto seq = [&](int r) { return Lbase + (uint32_t)(r - lo); };
@@ -274,24 +287,22 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
       return reinterpret_cast<const T *>(ring1 + (size_t)sl * PXB) + lane * NV;
     };
     int j = jb0, rel_next = lo, cum = 0;
-    wait_row(jb0 - 1);
-    wait_row(jb0);
-    wait_row(jb0 + 1);
+    for (int r = jb0 - Gm::HALO; r <= jb0 + Gm::HALO; r++) wait_row(r);
     RowMeta mc = meta[seq(j) % Q];
     for (int f = w;; f += NC) {
       while (f >= cum + (mc.c1 - mc.c0)) {      // advance the cursor to f's row
         cum += mc.c1 - mc.c0;
         if (++j >= jb1) break;
-        // this warp's remaining pixels lie in rows >= j: rows <= j-2 have had
-        // their last reader; release them before waiting for row j+1 (a warp
-        // must never hold old rows while it waits for new ones)
-        if (rel_next <= j - 2) {
+        // this warp's remaining pixels lie in rows >= j: rows <= j-1-HALO have
+        // had their last reader; release them before waiting for row j+HALO (a
+        // warp must never hold old rows while it waits for new ones)
+        if (rel_next <= j - 1 - Gm::HALO) {
           __syncwarp();
           if (lane == 0)
-            for (int r = rel_next; r <= j - 2; r++) mbar_arrive(&empty[seq(r) % Q]);
-          rel_next = j - 1;
+            for (int r = rel_next; r <= j - 1 - Gm::HALO; r++) mbar_arrive(&empty[seq(r) % Q]);
+          rel_next = j - Gm::HALO;
         }
-        wait_row(j + 1);
+        wait_row(j + Gm::HALO);
         mc = meta[seq(j) % Q];
       }
       if (j >= jb1) break;
@@ -299,7 +310,7 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
       const int a = mc.c0 + (f - cum);
       int sl2 = mc.p2 + (a - mc.c0);
       if (sl2 >= Gm::N2) sl2 -= Gm::N2;
-      const int4 nb = nbr_ring[sl2];
+      const int4 nb = nbr_ring[(size_t)sl2 * Gm::NBW];
       const T *ps = tile1(mc, a);
       T xs[D2][NV], acc[D2][NV], xn[D2][NV], z[D2][NV];
       if constexpr (HAS_ALPHA && !Gm::R2U) {
@@ -316,7 +327,62 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
         for (int e = 0; e < NV; e++) acc[k][e] = (T)0;
       // faces on the outer square under ABSORB (Eq. (4)) are marked -2
       const int outer = (nb.x == -2) | ((nb.y == -2) << 1) | ((nb.z == -2) << 2) | ((nb.w == -2) << 3);
-      if (__builtin_expect(outer == 0, 1)) {
+      if constexpr (is_quad<P>()) {
+        // N4 Q_p: self[code] + per open face the neighbour block (two variants:
+        // opposite face open / closed) and the far block of the pixel two
+        // steps on (when extracellular); the corners couple to nothing
+        const int4 nb2 = nbr_ring[(size_t)sl2 * Gm::NBW + 1];
+        const int code = open_code(nb);
+        mv_self<T, NV, P>(code, acc, xs);
+        if (nb.x >= 0) {
+          const T *pn = tile1(mc, nb.x);
+#pragma unroll
+          for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
+          if (nb.y >= 0) mv_imm<T, NV, P, 16>(acc, xn); else mv_imm<T, NV, P, 20>(acc, xn);
+          if (nb2.x >= 0) {
+            const T *pf = tile1(mc, nb2.x);
+#pragma unroll
+            for (int k = 0; k < D2; k++) lds<T, NV>(pf + k * G, xn[k]);
+            mv_imm<T, NV, P, 24>(acc, xn);
+          }
+        }
+        if (nb.y >= 0) {
+          const T *pn = tile1(mc, nb.y);
+#pragma unroll
+          for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
+          if (nb.x >= 0) mv_imm<T, NV, P, 17>(acc, xn); else mv_imm<T, NV, P, 21>(acc, xn);
+          if (nb2.y >= 0) {
+            const T *pf = tile1(mc, nb2.y);
+#pragma unroll
+            for (int k = 0; k < D2; k++) lds<T, NV>(pf + k * G, xn[k]);
+            mv_imm<T, NV, P, 25>(acc, xn);
+          }
+        }
+        if (nb.z >= 0) {
+          const T *pn = tile1(meta[seq(j + 1) % Q], nb.z);
+#pragma unroll
+          for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
+          if (nb.w >= 0) mv_imm<T, NV, P, 18>(acc, xn); else mv_imm<T, NV, P, 22>(acc, xn);
+          if (nb2.z >= 0) {
+            const T *pf = tile1(meta[seq(j + 2) % Q], nb2.z);
+#pragma unroll
+            for (int k = 0; k < D2; k++) lds<T, NV>(pf + k * G, xn[k]);
+            mv_imm<T, NV, P, 26>(acc, xn);
+          }
+        }
+        if (nb.w >= 0) {
+          const T *pn = tile1(meta[seq(j - 1) % Q], nb.w);
+#pragma unroll
+          for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
+          if (nb.z >= 0) mv_imm<T, NV, P, 19>(acc, xn); else mv_imm<T, NV, P, 23>(acc, xn);
+          if (nb2.w >= 0) {
+            const T *pf = tile1(meta[seq(j - 2) % Q], nb2.w);
+#pragma unroll
+            for (int k = 0; k < D2; k++) lds<T, NV>(pf + k * G, xn[k]);
+            mv_imm<T, NV, P, 27>(acc, xn);
+          }
+        }
+      } else if (__builtin_expect(outer == 0, 1)) {
         // self block of this pixel's open-face code (compile-time immediates),
         // then the fixed neighbour blocks of the open faces
         // (P3: 400-entry blocks; a 16-variant switch would not fit the

@@ -30,7 +30,8 @@ class dgdiff_opts(ctypes.Structure):
                 ("temporal_steps", ctypes.c_int32), ("device", ctypes.c_int32), ("rank", ctypes.c_int32),
                 ("nranks", ctypes.c_int32), ("nccl_id", ctypes.c_void_p), ("keep_density", ctypes.c_int32),
                 ("max_chunk", ctypes.c_int32), ("stream", ctypes.c_void_p), ("kernel", ctypes.c_int32),
-                ("mixture_radius", ctypes.c_int32), ("windows", ctypes.c_int32)]
+                ("mixture_radius", ctypes.c_int32), ("windows", ctypes.c_int32),
+                ("element", ctypes.c_int32)]
 
 
 class dgdiff_stats_t(ctypes.Structure):
@@ -155,8 +156,9 @@ def dgdiff_source_moments(handle, n):
     return out
 
 
-def dgdiff_get_density(handle, src, nx, ny, degree):
-    out = np.zeros((ny, nx, 2, ndof(degree)))
+def dgdiff_get_density(handle, src, nx, ny, degree, element=0):
+    """Canonical fp64 density: [ny][nx][2][d] (triangles) or [ny][nx][(p+1)^2] (quads)."""
+    out = np.zeros((ny, nx, 2, ndof(degree)) if element == 0 else (ny, nx, (degree + 1) ** 2))
     _check(lib.dgdiff_get_density(handle, int(src), _dp(out)))
     return out
 
@@ -275,7 +277,7 @@ class Solver:
         return dgdiff_mc_covariance(self.handle, sources, walkers_per_source, nsteps, delta, seed, want_disp)
 
     def density(self, src):
-        return dgdiff_get_density(self.handle, src, self.nx, self.ny, self.degree)
+        return dgdiff_get_density(self.handle, src, self.nx, self.ny, self.degree, self.opts.element)
 
     def stats(self):
         return dgdiff_get_stats(self.handle)

@@ -650,3 +650,67 @@ def test_points_at_centres_equal_pixel_sources(dg, cfg):
                 s.solve_points(np.array(bad, float), 1 / 32, 2)
             assert e.value.status == dg.E_SOURCE
     assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("p,prec", [(1, 64), (2, 64), (1, 32), (2, 32)])
+def test_quads_random_masks_vs_oracle(dg, orc, p, prec):
+    """N4 Q_p quadrilaterals (9-point-cross ring kernel: 2-column strip halo,
+    rows j-2..j+2, 8 neighbour indices) against O1's element-loop quad path
+    on a random walled mask with a ragged two-chunk batch."""
+    rng = np.random.default_rng(700 + 10 * p + prec)
+    ny, nx = 21, 25
+    m = (rng.random((ny, nx)) < 0.35).astype(np.uint8)
+    free = np.argwhere(m == 0)
+    G = 32 if prec == 64 else 64
+    n = G + 11
+    pick = free[rng.integers(0, len(free), n)]
+    src = np.stack([pick[:, 1], pick[:, 0]], 1).astype(np.int32)
+    h, D = 0.8, 1.4
+    dt = (1 / 16 if p == 1 else 1 / 64) * h * h / D
+    ref_m, ref_d = orc.q_solve(p, h, D, m, src, dt, 40, keep_density=True)
+    with dg.Solver(m, h, D, p, precision=prec, keep_density=1, max_chunk=G, element=1) as s:
+        s.solve(src, dt, 40)
+        S, mu = s.covariance()
+        mom = s.moments()
+        dens = {k: s.density(k) for k in range(G, n)}
+    t = TOL[prec]
+    for k, dk in dens.items():
+        assert rel_l2(dk, ref_d[k]) <= t["dens"], k
+    assert mom_err(mom, ref_m) <= t["mom"]
+    R, _ = orc.sigma(ref_m)
+    assert sig_err(S, R) <= t["sig"]
+
+
+def test_quads_closed_forms_rotation_and_windows(dg):
+    """Q1 / Q2 free space: Sigma = 2 D Delta I + h^2/12 I (Q1) and 2 D Delta I
+    (Q2); on a walled substrate a 90-degree rotation gives R Sigma R^T exactly
+    (quads are D4-symmetric); N1 windows are bitwise equal for quads too (the
+    support grows by two pixels per stage)."""
+    fm = np.zeros((96, 96), np.uint8)
+    src = np.array([[48, 48], [47, 49], [49, 46]], np.int32)
+    with dg.Solver(fm, 1.0, 1.0, 1, element=1) as s:
+        s.solve(src, 1 / 32, 16)
+        S1, _ = s.covariance()
+    assert np.abs(S1 - (1.0 + 1 / 12) * np.eye(2)).max() <= 1e-11
+    with dg.Solver(fm, 1.0, 1.0, 2, element=1) as s:
+        s.solve(src, 1 / 128, 64)
+        S2, _ = s.covariance()
+    assert np.abs(S2 - 1.0 * np.eye(2)).max() <= 1e-11
+    rng = np.random.default_rng(9)
+    m = (rng.random((40, 40)) < 0.4).astype(np.uint8)
+    free = np.argwhere(m[12:28, 12:28] == 0) + 12
+    ps = np.array([(f[1], f[0]) for f in free[:20]], np.int32)
+    n = m.shape[0]
+    with dg.Solver(m, 1.0, 1.0, 2, element=1) as s:
+        s.solve(ps, 1 / 128, 100)
+        S, _ = s.covariance()
+        mom0 = s.moments()
+    with dg.Solver(np.rot90(m).copy(), 1.0, 1.0, 2, element=1) as s:
+        s.solve(np.array([(j, n - 1 - i) for i, j in ps], np.int32), 1 / 128, 100)
+        Sr, _ = s.covariance()
+    Rm = np.array([[0, -1], [1, 0]])
+    assert np.allclose(Sr, Rm @ S @ Rm.T, rtol=1e-12, atol=1e-14)
+    with dg.Solver(m, 1.0, 1.0, 2, element=1, windows=1, max_chunk=32) as s:
+        s.solve(ps, 1 / 128, 100)
+        mom1 = s.moments()
+    assert np.array_equal(mom0, mom1)

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--config", default="c4")
     ap.add_argument("--tb", type=int, default=0)
     ap.add_argument("--windows", type=int, default=0)
+    ap.add_argument("--element", type=int, default=0)
     a = ap.parse_args()
     import torch
     torch.cuda.set_device(0)
@@ -32,9 +33,9 @@ def main():
     from paper_1907_06191_b200 import dgdiff as dg
     m = configs.mask(a.config)
     src = configs.sources(a.config)[:a.sources] if a.config != "c1" else configs.sources("c1")
-    dt = {1: 1 / 32, 2: 1 / 128, 3: 1 / 256}[a.degree]
+    dt = ({1: 1 / 16, 2: 1 / 64} if a.element else {1: 1 / 32, 2: 1 / 128, 3: 1 / 256})[a.degree]
     s = dg.Solver(m, 1.0, 1.0, a.degree, precision=a.precision, kernel=a.kernel, temporal_steps=a.tb,
-                  max_chunk=max(a.sources, 64), windows=a.windows)
+                  max_chunk=max(a.sources, 64), windows=a.windows, element=a.element)
     out = []
     for r in range(a.reps):
         dg.dgdiff_reset_stats(s.handle)
