@@ -95,7 +95,7 @@ struct RingGeom {
   static constexpr int NC = RingCfg<P, NV * (int)sizeof(T), ring_mode<P>(ALPHA)>::NC;
   static constexpr int PXB = D2 * G * (int)sizeof(T);  // one pixel tile (one group)
   static constexpr int SMEM_MAX = 232448;
-  static constexpr int EXTRA = 2 * RING_Q * 8 + RING_Q * 32 + (RING_MAXBAND + 2) * 16 + 2 * RING_Q * 4;
+  static constexpr int EXTRA = 2 * RING_Q * 8 + RING_Q * 32 + (RING_MAXBAND + 4) * 16 + 2 * RING_Q * 4;
   // ring 2 holds staged u0 tiles (R2U) and neighbour indices; otherwise it
   // only holds the 16-byte indices and ring 1 takes the rest
   static constexpr int N2 = R2U ? 4 * W : 16 * W;
@@ -106,7 +106,7 @@ struct RingGeom {
   static constexpr int OFF_BAR = OFF_NB + N2 * 16 * NBW;
   static constexpr int OFF_META = OFF_BAR + 2 * RING_Q * 8;
   static constexpr int OFF_RT = OFF_META + RING_Q * 32;
-  static constexpr int SMEM = OFF_RT + (RING_MAXBAND + 2) * 16 + 2 * RING_Q * 4;
+  static constexpr int SMEM = OFF_RT + (RING_MAXBAND + 4) * 16 + 2 * RING_Q * 4;   // rows of a band + 2 halos
   static constexpr int THREADS = (NC + 1) * 32;
   static_assert(SMEM <= SMEM_MAX, "ring does not fit in shared memory");
   static_assert(N1 >= ROWS_MIN * (W + 2 * HALO) && N2 >= ROWS_MIN * W, "rings too small for progress");
@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
     // issued at once (each lane arms its row's barrier and issues its own
     // bulk copies), and releases are awaited in row order only when the
     // rings are full.  rv1/rv2[q] = virtual end of the row in entry q.
-    uint32_t *rv = reinterpret_cast<uint32_t *>(rt + RING_MAXBAND + 2);   // [2][Q]
+    uint32_t *rv = reinterpret_cast<uint32_t *>(rt + RING_MAXBAND + 4);   // [2][Q]
     uint32_t L = 0;                 // row loads issued by this CTA
     uint32_t v1 = 0, v2 = 0;        // virtual slot counters of rings 1 and 2
     uint32_t rel = 0;               // rows whose release has been observed
@@ -489,9 +489,11 @@ cudaError_t launch_ring(const dgl::StageArgs &a) {
       (const T *)a.Uin, (const T *)a.U0, (T *)a.Uout, a.nbr, ALPHA ? a.rowtab : a.rowtab_na, a.nact, a.ny,
       ALPHA ? a.nstrips : a.nstrips_na, a.ngroups,
       band_rows, nitems, (T)a.alpha, (T)a.cs, a.diag,
-      std::max(4, std::min(RING_Q - 1, alpha_max_ahead(a, ALPHA))),
-      Gm::R2U ? Gm::N1 : std::max(4 * (Gm::W + 2), std::min(Gm::N1, a.n1_use_na > 0 ? a.n1_use_na : Gm::N1)),
-      std::max(4 * Gm::W, std::min(Gm::N2, a.n2_use > 0 ? a.n2_use : Gm::N2)), (const T *)a.Aabs, a.gbox, a.wr);
+      std::max(Gm::ROWS_MIN, std::min(RING_Q - 1, alpha_max_ahead(a, ALPHA))),
+      // (never below the progress minimum: ROWS_MIN full halo'd rows)
+      Gm::R2U ? Gm::N1
+              : std::max(Gm::ROWS_MIN * (Gm::W + 2 * Gm::HALO), std::min(Gm::N1, a.n1_use_na > 0 ? a.n1_use_na : Gm::N1)),
+      std::max(Gm::ROWS_MIN * Gm::W, std::min(Gm::N2, a.n2_use > 0 ? a.n2_use : Gm::N2)), (const T *)a.Aabs, a.gbox, a.wr);
   return cudaGetLastError();
 }
 
