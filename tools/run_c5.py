@@ -17,6 +17,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--nsteps", type=int, default=100000)
     ap.add_argument("--precision", type=int, default=64)
+    ap.add_argument("--element", type=int, default=0, help="1 = quadrilateral Q2 (N4)")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -26,7 +27,7 @@ def main():
     m = configs.mask("c5")
     src = configs.sources("c5")
     st = torch.cuda.current_stream()
-    s = dg.Solver(m, 1.0, 1.0, 2, precision=a.precision, stream=st.cuda_stream)
+    s = dg.Solver(m, 1.0, 1.0, 2, precision=a.precision, stream=st.cuda_stream, element=a.element)
     dt = 1 / 128
     s.solve(src, dt, 10)                       # warm-up
     s.covariance()
@@ -43,9 +44,9 @@ def main():
     stt = s.stats()
     mom = s.moments()
     ny, nx = m.shape
-    dofs = 2 * nx * ny * 6
+    dofs = nx * ny * (9 if a.element else 12)
     delta = a.nsteps * dt
-    out = dict(config="c5", grid=[nx, ny], degree=2, precision=a.precision, sources=len(src), nsteps=a.nsteps,
+    out = dict(config="c5", grid=[nx, ny], degree=2, element="Q2" if a.element else "P2", precision=a.precision, sources=len(src), nsteps=a.nsteps,
                dt=dt, delta=delta, device_ms=ms, wall_s=time.time() - w0,
                element_dof_updates_per_s=len(src) * dofs * a.nsteps / (ms * 1e-3),
                stage_gbs=stt["stage_bytes"] / (stt["stage_ms"] * 1e-3) / 1e9,
