@@ -588,3 +588,29 @@ def test_quad_rotation_90_and_transpose_exact(orc):
     St, _ = orc.sigma(orc.q_solve(2, 1.0, 1.0, mask.T.copy(), [(j, i) for i, j in src], 1 / 128, 120))
     assert np.allclose(St, S[::-1, ::-1], rtol=1e-12, atol=1e-14)
     assert np.linalg.eigvalsh(S).min() > 0
+
+
+@pytest.mark.parametrize("p,rho", [(1, 60.0), (2, 192.7953), (3, 462.37)])
+def test_spectral_radius_bounds_pin_dt_max(orc, p, rho):
+    """The library's dt limits are 2.5127453 / rho_p.  Pin rho_p
+    against the assembled operator: the Bloch symbol of the all-open
+    composite blocks (interior modes), a free grid with walls on all four
+    sides (wall modes reach slightly above the interior sup for P2/P3) and
+    random masks all stay inside rho_p, and rho_p is within 1 % of the
+    largest of them (a constant far too large would waste steps, one too
+    small would make dt_max unstable)."""
+    blocks, stray = O2.composite_blocks(p, 15)
+    assert stray < 1e-10
+    seen = 0.0
+    for tx in np.linspace(0, np.pi, 41):
+        for ty in np.linspace(0, np.pi, 41):
+            S = sum(B * np.exp(1j * (tx * o[0] + ty * o[1])) for o, B in blocks.items())
+            seen = max(seen, np.abs(np.linalg.eigvals(S)).max())
+    rng = np.random.default_rng(3)
+    for n, f in ((12, 0.0), (7, 0.2), (7, 0.4)):
+        mask = (rng.random((n, n)) < f).astype(np.uint8)
+        lam = np.linalg.eigvals(O2.assemble(p, 1.0, 1.0, mask))
+        assert lam.real.max() < 1e-9
+        seen = max(seen, np.abs(lam).max())
+    assert seen <= rho * (1 + 1e-9), seen
+    assert rho <= 1.01 * seen, seen
