@@ -614,3 +614,24 @@ def test_spectral_radius_bounds_pin_dt_max(orc, p, rho):
         seen = max(seen, np.abs(lam).max())
     assert seen <= rho * (1 + 1e-9), seen
     assert rho <= 1.01 * seen, seen
+
+
+@pytest.mark.parametrize("p,rho", [(1, 32.0), (2, 130.7)])
+def test_quad_spectral_radius_pins_dt_max(orc, p, rho):
+    """Quads (R22): the library's Q_p dt limit 2.5127453 / rho uses the Bloch
+    radius of the 9-point-cross symbol; walled and random-mask operators stay
+    inside it and rho is within 1 % of what is seen."""
+    from oracle import dense_quad as Q
+    B = Q.composite_blocks(p, 15)
+    offs = [k for k, v in B.items() if np.abs(v).max() > 1e-12]
+    seen = 0.0
+    for tx in np.linspace(0, np.pi, 61):
+        for ty in np.linspace(0, np.pi, 61):
+            S = sum(B[o] * np.exp(1j * (tx * o[0] + ty * o[1])) for o in offs)
+            seen = max(seen, np.abs(np.linalg.eigvals(S)).max())
+    rng = np.random.default_rng(4)
+    for n, f in ((10, 0.0), (7, 0.3)):
+        lam = np.linalg.eigvals(Q.assemble(p, 1.0, 1.0, (rng.random((n, n)) < f).astype(np.uint8)))
+        assert lam.real.max() < 1e-9
+        seen = max(seen, np.abs(lam).max())
+    assert seen <= rho and rho <= 1.01 * seen, seen
