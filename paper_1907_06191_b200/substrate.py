@@ -183,9 +183,9 @@ def save_substrate(path, sub: Substrate, k0=450.0):
     """SPEC S:93 text format: '# substrate side=<L> k0=<k0>', then 'x,y,r' lines."""
     ny, nx = sub.mask.shape
     with open(path, "w") as f:
-        f.write(f"# substrate side={nx * sub.h_um!r} k0={k0!r}\n")
-        for x, y, r in sub.circles:
-            f.write(f"{x!r},{y!r},{r!r}\n")
+        f.write(f"# substrate side={float(nx * sub.h_um)!r} k0={float(k0)!r}\n")
+        for x, y, r in sub.circles:   # repr of a Python float round-trips exactly
+            f.write(f"{float(x)!r},{float(y)!r},{float(r)!r}\n")
 
 
 def load_circles(path):
