@@ -68,7 +68,7 @@ template <> struct RingCfg<2, 8, RING_PLAIN> { static constexpr int W = 16, NC =
 template <> struct RingCfg<2, 8, RING_U0_STAGED> { static constexpr int W = 8, NC = 16; };
 template <> struct RingCfg<2, 8, RING_U0_DIRECT> { static constexpr int W = 16, NC = 12; };   // c5: NC 8 -> 12 -4 %
 // P3 (N4): 5 KB pixel tiles (fp64), four halo'd rows of W = 8 fill ring 1
-template <> struct RingCfg<3, 8, RING_PLAIN> { static constexpr int W = 8, NC = 8; };
+template <> struct RingCfg<3, 8, RING_PLAIN> { static constexpr int W = 8, NC = 12; };   // c5: NC 8 -> 12 -10 %
 template <> struct RingCfg<3, 8, RING_U0_STAGED> { static constexpr int W = 8, NC = 8; };
 template <> struct RingCfg<3, 8, RING_U0_DIRECT> { static constexpr int W = 8, NC = 8; };
 // N4 quadrilaterals: degree codes 101 (Q1), 102 (Q2); their composite
