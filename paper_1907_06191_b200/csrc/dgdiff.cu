@@ -56,8 +56,11 @@ static dgdiff_status fail(dgdiff_status s, const char *fmt, ...) {
 // device constants
 // ---------------------------------------------------------------------------
 #define DMAXK 10                   // max dofs per triangle on the GPU path (P3)
-__constant__ double c_W[2 * 6 * DMAXK];    // moment weights (unit pixel)
-__constant__ double c_CW[2 * DMAXK];       // basis values at the pixel centre (mixture nodes)
+// per-handle tables passed by value as kernel parameters (they live in the
+// launch's constant bank; a module-wide __constant__ would be shared by every
+// handle of the process, whatever its degree / element type)
+struct MomW { double w[2 * 6 * DMAXK]; };   // moment weights (unit pixel)
+struct CentreW { double v[2 * DMAXK]; };    // basis values at the pixel centre (mixture nodes)
 
 struct InitVals { double v[2 * DMAXK]; };  // projected Dirac / h^2
 
@@ -133,7 +136,8 @@ template <typename T, int NV, int D2>
 __global__ void __launch_bounds__(256) k_moments(const T *__restrict__ U, const int2 *__restrict__ pix,
                                                  const double2 *__restrict__ src_xy, int nact, int ngroups,
                                                  int px_per_cta, double *__restrict__ partial,
-                                                 int64_t chunk, const int2 *__restrict__ grange /* nullable (N1) */) {
+                                                 int64_t chunk, const int2 *__restrict__ grange /* nullable (N1) */,
+                                                 MomW mw) {
   constexpr int NT = (D2 == 4 || D2 == 9) ? 1 : 2;   // elements per pixel (quads: 1)
   constexpr int G = 32 * NV, d = D2 / NT;
   const int lane = threadIdx.x & 31;
@@ -169,7 +173,7 @@ __global__ void __launch_bounds__(256) k_moments(const T *__restrict__ U, const 
 #pragma unroll
         for (int q = 0; q < 6; q++)
 #pragma unroll
-          for (int j = 0; j < d; j++) P[q] = fma(c_W[(t * 6 + q) * DMAXK + j], (double)c[t * d + j][e], P[q]);
+          for (int j = 0; j < d; j++) P[q] = fma(mw.w[(t * 6 + q) * DMAXK + j], (double)c[t * d + j][e], P[q]);
       const double X = ij.x - is[e], Y = ij.y - js[e];
       m[0][e] += P[0];
       m[1][e] += P[1] + X * P[0];
@@ -296,7 +300,8 @@ __global__ void k_src_prep(const int32_t *__restrict__ src, int64_t nvalid, int6
 template <typename T, int NV, int D2>
 __global__ void k_mixture(const T *__restrict__ U, const int *__restrict__ aidx, int nx, int ny, int nact,
                           const int2 *__restrict__ src_ij, const double *__restrict__ mom, int64_t nvalid, int R,
-                          double *__restrict__ grid, const int2 *__restrict__ grange /* nullable (N1) */) {
+                          double *__restrict__ grid, const int2 *__restrict__ grange /* nullable (N1) */,
+                          CentreW cw) {
   constexpr int NT = (D2 == 4 || D2 == 9) ? 1 : 2;
   constexpr int G = 32 * NV, d = D2 / NT;
   const int side = 2 * R + 1;
@@ -320,8 +325,8 @@ __global__ void k_mixture(const T *__restrict__ U, const int *__restrict__ aidx,
     double vl = 0.0, vu = 0.0;
 #pragma unroll
     for (int k = 0; k < d; k++) {
-      vl += c_CW[k] * (double)p[(size_t)k * G];
-      if (NT == 2) vu += c_CW[DMAXK + k] * (double)p[(size_t)(d + k) * G];
+      vl += cw.v[k] * (double)p[(size_t)k * G];
+      if (NT == 2) vu += cw.v[DMAXK + k] * (double)p[(size_t)(d + k) * G];
     }
     acc += (NT == 2 ? 0.5 * (vl + vu) : vl) / mom[s * 6];   // quads: one element, its centre value
   }
@@ -426,6 +431,8 @@ struct dgdiff_s {
   int64_t mom_cap = 0;
   double *d_out = nullptr;
   // N1 active windows
+  MomW momw;                                       // this handle's moment weights (kernel parameter)
+  CentreW centw;                                   // and mixture node weights
   bool windows = false;
   bool quad = false;                               // N4 quadrilateral Q_p elements (opts.element = 1)
   int halo = 1;                                    // composite stencil reach (quads: 2)
@@ -830,11 +837,11 @@ static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
     for (int q = 0; q < 6; q++)
       for (int j = 0; j < H->d; j++) W[(t * 6 + q) * DMAXK + j] = H->tab.W[(t * 6 + q) * H->d + j];
   // (quads: H->d = D2, t = 1 rows are zero and unused)
-  CK(cudaMemcpyToSymbol(c_W, W, sizeof W));
+  memcpy(H->momw.w, W, sizeof W);
   double CWv[2 * DMAXK] = {0};
   for (int t = 0; t < 2; t++)
     for (int j = 0; j < H->d; j++) CWv[t * DMAXK + j] = H->tab.cw[t * H->d + j];
-  CK(cudaMemcpyToSymbol(c_CW, CWv, sizeof CWv));
+  memcpy(H->centw.v, CWv, sizeof CWv);
   if (H->o.mixture_radius > 0) {
     H->mix_R = H->o.mixture_radius;
     const size_t nc = (size_t)(2 * H->mix_R + 1) * (2 * H->mix_R + 1);
@@ -1099,7 +1106,7 @@ after_stepping:
   }
   dim3 mgrid(nblk, (ngroups + wpb - 1) / wpb);
   k_moments<T, NV, D2><<<mgrid, 32 * wpb, 0, st>>>(u, H->d_pix, H->d_src_xy, nact, ngroups, mpx, H->d_partial,
-                                               chunk, H->windows ? H->d_grange : nullptr);
+                                               chunk, H->windows ? H->d_grange : nullptr, H->momw);
   k_mom_reduce<<<(int)((nvalid + 127) / 128), 128, 0, st>>>(H->d_partial, nblk, chunk, nvalid, H->h, mom_rows,
                                                             H->windows ? H->d_perm + H->last_chunk_pos0 : nullptr,
                                                             H->d_mom);
@@ -1108,7 +1115,7 @@ after_stepping:
     const int nc = (2 * H->mix_R + 1) * (2 * H->mix_R + 1);
     k_mixture<T, NV, D2><<<(nc + 127) / 128, 128, 0, st>>>(u, H->d_aidx, H->nx, H->ny, nact, H->d_src_ij, mom_rows,
                                                          nvalid, H->mix_R, H->d_mix,
-                                                         H->windows ? H->d_grange : nullptr);
+                                                         H->windows ? H->d_grange : nullptr, H->centw);
     H->st.launches++;
   }
   CK(cudaGetLastError());

@@ -31,6 +31,7 @@
 // issued while rows j-1 and j are held (no deadlock).
 #pragma once
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include "kernels.cuh"
 #include "stage_imm.cuh"
@@ -467,15 +468,20 @@ inline int alpha_max_ahead(const dgl::StageArgs &a, bool alpha) {
 template <typename T, int NV, int P, bool ALPHA>
 cudaError_t launch_ring(const dgl::StageArgs &a) {
   using Gm = RingGeom<T, NV, P, ALPHA>;
-  static bool attr = false;
-  static int pad = 0;
-  if (!attr) {
-    if (const char *e = getenv("DGDIFF_SMEM_PAD")) pad = atoi(e);
-    if (Gm::SMEM + pad > Gm::SMEM_MAX) pad = Gm::SMEM_MAX - Gm::SMEM;
+  // the dynamic shared-memory opt-in is per device: one bit per ordinal
+  static std::atomic<uint64_t> attr_set{0};
+  static const int pad = [] {
+    int v = 0;
+    if (const char *e = getenv("DGDIFF_SMEM_PAD")) v = atoi(e);
+    return Gm::SMEM + v > Gm::SMEM_MAX ? Gm::SMEM_MAX - Gm::SMEM : std::max(0, v);
+  }();
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+  if (!(attr_set.load() >> dev & 1)) {
     cudaError_t e = cudaFuncSetAttribute(k_stage_ring<T, NV, P, ALPHA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Gm::SMEM + pad);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr_set.fetch_or(uint64_t(1) << dev);
   }
   const int per_band = (ALPHA ? a.nstrips : a.nstrips_na) * a.ngroups;
   int nbands = std::max(1, std::min(a.ny, (8 * a.nsm + per_band - 1) / per_band));

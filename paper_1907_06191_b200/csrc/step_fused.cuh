@@ -23,6 +23,7 @@
 // rowtab3[s][r] = {h0, a1, a2, c0} {c1, b2, b1, h1}: active-index bounds of
 // the u / U1 / U2 / output ranges of strip s, row r.
 #pragma once
+#include <atomic>
 #include <algorithm>
 #include <cstdlib>
 
@@ -382,11 +383,13 @@ __global__ void __launch_bounds__(FusedGeom<T>::THREADS, 1)
 template <typename T>
 cudaError_t launch_fused(const dgl::StageArgs &a) {
   using Gm = FusedGeom<T>;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr_set{0};   // per-device opt-in, one bit per ordinal
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+  if (!(attr_set.load() >> dev & 1)) {
     cudaError_t e = cudaFuncSetAttribute(k_step_fused<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, Gm::SMEM);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr_set.fetch_or(uint64_t(1) << dev);
   }
   const int per_band = a.nstrips * a.ngroups;
   int nbands = std::max(1, std::min(a.ny, (8 * a.nsm + per_band - 1) / per_band));

@@ -714,3 +714,28 @@ def test_quads_closed_forms_rotation_and_windows(dg):
         s.solve(ps, 1 / 128, 100)
         mom1 = s.moments()
     assert np.array_equal(mom0, mom1)
+
+
+def test_handles_are_independent(dg, cfg):
+    """Handles of different degree / element type alive at once give exactly
+    the moments each gives alone (no process-wide tables: the moment and
+    mixture weights travel with the handle)."""
+    m = cfg.mask("c1")
+    src = cfg.sources("c1")
+    alone = {}
+    for key in ((1, 0), (2, 0), (2, 1)):
+        with dg.Solver(m, 1.0, 1.0, key[0], element=key[1], mixture_radius=3) as s:
+            s.solve(src, 1 / 256, 20)
+            s.covariance()
+            alone[key] = (s.moments(), s.mixture()[0])
+    hs = {key: dg.Solver(m, 1.0, 1.0, key[0], element=key[1], mixture_radius=3) for key in alone}
+    try:
+        for key in ((2, 1), (1, 0), (2, 0)):      # created in one order, solved in another
+            hs[key].solve(src, 1 / 256, 20)
+        for key, h in hs.items():
+            h.covariance()
+            assert np.array_equal(h.moments(), alone[key][0]), key
+            assert np.array_equal(h.mixture()[0], alone[key][1]), key
+    finally:
+        for h in hs.values():
+            h.close()
