@@ -739,3 +739,25 @@ def test_handles_are_independent(dg, cfg):
     finally:
         for h in hs.values():
             h.close()
+
+
+@pytest.mark.parametrize("p,element", [(1, 0), (2, 0), (3, 0), (1, 1), (2, 1)])
+def test_degenerate_grids(dg, orc, p, element):
+    """Edge cases of the substrate shape: a single pixel (no open face: the
+    density must not move), a one-pixel-high strip (1-D diffusion; the ring
+    kernel's bands and halos collapse), every source on the same pixel, and
+    zero steps -- against the oracle (triangles or quads), with and without
+    N1 windows."""
+    solve = orc.solve if element == 0 else orc.q_solve
+    dt = {1: 1 / 32, 2: 1 / 128, 3: 1 / 256}[p] if element == 0 else {1: 1 / 16, 2: 1 / 64}[p]
+    for shape, src in (((1, 1), [(0, 0)]), ((1, 37), [(5, 0), (5, 0), (36, 0)]), ((29, 2), [(1, 28), (0, 0)])):
+        m = np.zeros(shape, np.uint8)
+        for nsteps in (0, 7):
+            ref = solve(p, 1.0, 1.0, m, src, dt, nsteps)
+            for w in (0, 1):
+                with dg.Solver(m, 1.0, 1.0, p, element=element, windows=w) as s:
+                    s.solve(np.array(src, np.int32), dt, nsteps)
+                    mom = s.moments()
+                # (absolute: the P2+ second moments of the projected Dirac are 0)
+                assert np.abs(mom - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max()), (shape, nsteps, w)
+                assert np.abs(mom[:, 0] - 1).max() <= 1e-13
