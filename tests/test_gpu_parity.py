@@ -761,3 +761,20 @@ def test_degenerate_grids(dg, orc, p, element):
                 # (absolute: the P2+ second moments of the projected Dirac are 0)
                 assert np.abs(mom - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max()), (shape, nsteps, w)
                 assert np.abs(mom[:, 0] - 1).max() <= 1e-13
+
+
+def test_c4_device_filling_chunk_and_ragged_tail(dg, orc, cfg):
+    """Maximum size: the c4 substrate with the chunk sized by free device
+    memory (~640 sources, ~155 GB of RK registers on a B200) and a ragged
+    second chunk; sources sampled in both chunks against O1 (2 steps)."""
+    m = cfg.mask("c4")
+    src = cfg.sources("c4", 1000)[:700]
+    with dg.Solver(m, 1.0, 1.0, 1) as s:
+        s.solve(src, 1 / 32, 2)
+        mom = s.moments()
+        st = s.stats()
+    assert 256 < st["chunk"] < 700                    # memory-limited chunk, so there is a tail
+    pick = np.array([1, st["chunk"] + 3])
+    ref = orc.solve(1, 1.0, 1.0, m, src[pick], 1 / 32, 2)
+    assert mom_err(mom[pick], ref) <= 1e-10
+    assert np.abs(mom[:, 0] - 1).max() <= 1e-13
