@@ -94,7 +94,14 @@ typedef struct {
                              zero (results agree with windows = 0 to
                              rounding; moments are returned in input order).
                              Ring kernel only (kernel 1/2, temporal_steps 2 ->
-                             E_ARG).  0 (default) = whole grid */
+                             E_ARG).  2 = the same, with each box's growth
+                             also capped at K sigma = K sqrt(2 D t) / h
+                             (+ one stencil reach), K = 20 (P1), 25 (Q1), 30 (P2),
+                             40 (Q2), 45 (P3): the DG density's tails are
+                             below fp64 rounding there (DESIGN R23),
+                             so results agree with the whole-grid solve to
+                             ~1e-14 but are no longer bitwise equal.
+                             0 (default) = whole grid */
   int32_t element;        /* 0 (default) = two P_p triangles per pixel;
                              1 = one Q_p quadrilateral per pixel (N4, the north
                              star's "Q2"; degree 1 or 2): tensor Lagrange basis

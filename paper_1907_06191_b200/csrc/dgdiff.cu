@@ -434,6 +434,8 @@ struct dgdiff_s {
   MomW momw;                                       // this handle's moment weights (kernel parameter)
   CentreW centw;                                   // and mixture node weights
   bool windows = false;
+  bool win_apx = false;                            // windows = 2: clip the boxes at win_k sigma (F7)
+  double win_k = 20.0;                             // (env DGDIFF_WINK overrides; experiments)
   bool quad = false;                               // N4 quadrilateral Q_p elements (opts.element = 1)
   int halo = 1;                                    // composite stencil reach (quads: 2)
   int32_t *d_srcw = nullptr, *d_perm = nullptr;   // sorted local sources [nloc][2], their global indices
@@ -861,7 +863,13 @@ static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
     if (r != ncclSuccess) return fail(DGDIFF_E_NCCL, "ncclCommInitRank: %s", g_nccl.errStr(r));
   }
   H->st.n_active = H->nact;
-  H->windows = H->o.windows == 1;
+  H->windows = H->o.windows == 1 || H->o.windows == 2;
+  H->win_apx = H->o.windows == 2;
+  // clip factor per element type (reading R23, measured with
+  // tools/sweep_wink.py: max relative moment error <= 1e-14 against the
+  // whole-grid solve on c3): P1 20, P2 30, P3 45, Q1 25, Q2 40 sigma
+  H->win_k = H->quad ? (H->p == 1 ? 25.0 : 40.0) : (H->p == 1 ? 20.0 : H->p == 2 ? 30.0 : 45.0);
+  if (const char *wk = getenv("DGDIFF_WINK")) H->win_k = atof(wk);
   if (H->windows) {
     // 2-D prefix counts of extracellular pixels: algorithmic bytes of windowed stages
     H->h_pre.assign((size_t)(ny + 1) * (nx + 1), 0);
@@ -894,10 +902,10 @@ extern "C" dgdiff_status dgdiff_create(dgdiff_t *out, const uint8_t *mask, int32
   if (o.outer_bc != 0 && o.outer_bc != 1) return fail(DGDIFF_E_ARG, "outer_bc must be 0 (REFLECT) or 1 (ABSORB)");
   if (o.outer_bc == 1 && (o.kernel == 1 || o.kernel == 2 || o.temporal_steps == 2))
     return fail(DGDIFF_E_ARG, "outer_bc ABSORB runs on the default ring kernel only");
-  if (o.windows != 0 && o.windows != 1) return fail(DGDIFF_E_ARG, "windows must be 0 or 1");
+  if (o.windows < 0 || o.windows > 2) return fail(DGDIFF_E_ARG, "windows must be 0, 1 or 2");
   if (degree == 3 && (o.kernel == 1 || o.kernel == 2 || o.temporal_steps == 2 || o.outer_bc != 0))
     return fail(DGDIFF_E_ARG, "P3 (N4) runs on the default ring kernel with REFLECT only");
-  if (o.windows == 1 && (o.kernel == 1 || o.kernel == 2 || o.temporal_steps == 2))
+  if (o.windows != 0 && (o.kernel == 1 || o.kernel == 2 || o.temporal_steps == 2))
     return fail(DGDIFF_E_ARG, "windows (N1) run on the default ring kernel only");
   if (o.centering != 0 && o.centering != 1) return fail(DGDIFF_E_ARG, "centering must be 0 or 1");
   if (o.element != 0 && o.element != 1) return fail(DGDIFF_E_ARG, "element must be 0 (triangles) or 1 (quadrilaterals)");
@@ -934,6 +942,18 @@ extern "C" dgdiff_status dgdiff_create(dgdiff_t *out, const uint8_t *mask, int32
 // algorithmic flops of one SSP-RK3 step for `chunk` sources: 3 stages of the
 // structural MACs (2 flops each) plus the RK combinations per dof (stage 1:
 // 1 FMA = 2 flops; stages 2, 3: sub + FMA + FMA = 5 flops)
+// N1 window radius (pixels) after `stages` RK stages ending at time t: the
+// exact support reach (halo pixels per stage) or, for windows = 2, at most
+// K sigma = K sqrt(2 D t) / h (+ one stencil reach), K per element type
+// (R23): the DG tails are below rounding there (SURVEY F7 measured ~15 sigma
+// for P1; higher degrees have longer tails)
+static int64_t win_radius(const dgdiff_s *H, int64_t stages, double t) {
+  const int64_t exact = H->halo * stages;
+  if (!H->win_apx) return exact;
+  const int64_t apx = (int64_t)std::ceil(H->win_k * std::sqrt(2.0 * H->D * t) / H->h) + 2 * H->halo;
+  return std::min(exact, apx);
+}
+
 static double fused_flops_per_step(const dgdiff_s *H, int64_t chunk) {
   const double dofs = (double)H->nact * H->D2;
   return (double)chunk * (3.0 * 2.0 * H->macs_per_stage + dofs * (2.0 + 5.0 + 5.0));
@@ -1035,7 +1055,8 @@ static dgdiff_status run_chunk(dgdiff_s *H, int64_t nvalid, int64_t chunk, doubl
     sa.alpha = alpha;
     sa.cs = cs;
     if (H->windows) {
-      sa.wr = (int)std::min<int64_t>(1 << 30, H->halo * (3 * cur_step + k + 1));   // output support radius
+      // output support radius (exact reach, or the 15-sigma clip)
+      sa.wr = (int)std::min<int64_t>(1 << 30, win_radius(H, 3 * cur_step + k + 1, (double)(cur_step + 1) * dt));
       double px = 0;
       for (int g = 0; g < ngroups; g++) px += box_px(g, sa.wr);
       win_bytes += (k == 0 ? 2.0 : 3.0) * px * D2 * G * sizeof(T);
@@ -1308,7 +1329,7 @@ static dgdiff_status solve_impl(dgdiff_s *H, const int32_t *sources, const doubl
         // maintained active range per group: whole rows the group's stages can
         // read, [y0 - R - 1, y1 + R + 1] with R = 3 nsteps (raster order: contiguous)
         std::vector<int2> rng(ng);
-        const int64_t R = std::min<int64_t>(H->halo * (3 * nsteps + 1), H->ny);
+        const int64_t R = std::min<int64_t>(win_radius(H, 3 * nsteps, (double)nsteps * dt) + H->halo, H->ny);
         for (int64_t g = 0; g < ng; g++) {
           const int y0 = (int)std::max<int64_t>(0, H->h_gbox[g].z - R);
           const int y1 = (int)std::min<int64_t>(H->ny, H->h_gbox[g].w + R + 1);

@@ -778,3 +778,24 @@ def test_c4_device_filling_chunk_and_ragged_tail(dg, orc, cfg):
     ref = orc.solve(1, 1.0, 1.0, m, src[pick], 1 / 32, 2)
     assert mom_err(mom[pick], ref) <= 1e-10
     assert np.abs(mom[:, 0] - 1).max() <= 1e-13
+
+
+@pytest.mark.parametrize("p,element", [(1, 0), (2, 0), (3, 0), (1, 1), (2, 1)])
+def test_windows_sigma_clip(dg, cfg, p, element):
+    """N1 approximate windows (windows = 2, reading R23): the box growth is
+    capped at K sigma (K = 20 / 30 / 45 for P1 / P2 / P3, 25 / 40 for Q1 /
+    Q2), where the DG tails are below rounding: moments and Sigma agree with
+    the whole-grid solve to 1e-12 although far fewer bytes move."""
+    m = cfg.mask("c3")
+    src = cfg.sources("c3")[:300]
+    dt = ({1: 1 / 32, 2: 1 / 128, 3: 1 / 256} if element == 0 else {1: 1 / 16, 2: 1 / 64})[p]
+    nst = 300
+    res = {}
+    for w in (0, 2):
+        with dg.Solver(m, 1.0, 1.0, p, windows=w, element=element) as s:
+            s.solve(src, dt, nst)
+            S, mu = s.covariance()
+            res[w] = (s.moments(), S, s.stats()["stage_bytes"])
+    assert mom_err(res[2][0], res[0][0]) <= 1e-12
+    assert np.abs(res[2][1] - res[0][1]).max() <= 1e-12 * res[0][1].max()
+    assert res[2][2] < res[0][2]
