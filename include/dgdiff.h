@@ -145,8 +145,9 @@ dgdiff_status dgdiff_solve_batch(dgdiff_t, const int32_t *sources, int64_t n, do
  *         point on a pixel edge goes to the pixel above / right of it:
  *         DESIGN.md reading R21); its Dirac is L2-projected onto the triangle
  *         containing it (L: eta < xi, U: eta > xi; on the diagonal split 1/2 -
- *         1/2 as for pixel centres, R10), and its moments are taken about the
- *         point itself (R12).  A point at a pixel centre reproduces
+ *         1/2 as for pixel centres, R10) -- for quadrilaterals (element = 1)
+ *         onto the pixel's single element -- and its moments are taken about
+ *         the point itself (R12).  A point at a pixel centre reproduces
  *         dgdiff_solve_batch exactly.  E_SOURCE: non-finite, outside the grid
  *         or in an axon pixel.  The mixture lattice (dgdiff_mixture) is not
  *         accumulated for point sources (-> E_STATE there). */

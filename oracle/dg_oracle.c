@@ -1071,9 +1071,29 @@ static void q_project_delta(const qprob_t *P, int is, int js, double *u) {
   }
 }
 
-static void q_moments(const qprob_t *P, const double *u, int is, int js, double m[6]) {
+/* sub-pixel point (xi, eta) of pixel (is, js) (N4, reading R21): M u_K = N(xi, eta) */
+static void q_project_point(const qprob_t *P, int is, int js, double xi, double eta, double *u) {
   const qref_t *R = &P->R;
-  const double h = R->h, xs = (is + 0.5) * h, ys = (js + 0.5) * h;
+  memset(u, 0, sizeof(double) * (size_t)P->nx * P->ny * R->d);
+  double phi[QDMAX];
+  qbasis(R->p, xi, eta, phi, NULL);
+  double *uK = u + qidx(P, is, js);
+  for (int a = 0; a < R->d; a++) {
+    double s = 0.0;
+    for (int b = 0; b < R->d; b++) s += R->Minv[a][b] * phi[b];
+    uK[a] = s;
+  }
+}
+
+static void q_moments_about(const qprob_t *P, const double *u, double xs, double ys, double m[6]);
+
+static void q_moments(const qprob_t *P, const double *u, int is, int js, double m[6]) {
+  q_moments_about(P, u, (is + 0.5) * P->R.h, (js + 0.5) * P->R.h, m);
+}
+
+static void q_moments_about(const qprob_t *P, const double *u, double xs, double ys, double m[6]) {
+  const qref_t *R = &P->R;
+  const double h = R->h;
   for (int k = 0; k < 6; k++) m[k] = 0.0;
   for (int j = 0; j < P->ny; j++)
     for (int i = 0; i < P->nx; i++) {
@@ -1162,6 +1182,44 @@ int orc_q_solve(int p, double h, double D, int nx, int ny, const uint8_t *mask, 
       q_ssprk3_step(P, u, buf + ne, buf + 2 * ne, buf + 3 * ne, buf + 4 * ne, dt);
     double m[6];
     q_moments(P, u, is, js, m);
+    for (int k = 0; k < 6; k++) {
+      mom_out[s * 6 + k] = m[k];
+      if (!isfinite(m[k])) bad |= 1;
+    }
+    if (dens_out) memcpy(dens_out + (size_t)s * ne, u, sizeof(double) * ne);
+    free(buf);
+  }
+  free(P);
+  return bad ? 4 : 0;
+}
+
+/* orc_q_solve for physical point sources (N4; R21): pixel (floor(x/h),
+ * floor(y/h)), Dirac projected at the point, moments about the point */
+int orc_q_solve_points(int p, double h, double D, int nx, int ny, const uint8_t *mask, const double *points,
+                       int64_t n, double dt, int64_t nsteps, double *mom_out, double *dens_out, int nthreads) {
+  qprob_t *P = (qprob_t *)malloc(sizeof(qprob_t));
+  if (q_setup(P, p, h, D, nx, ny, mask) || n < 0 || nsteps < 0 || !(dt >= 0)) { free(P); return 1; }
+  for (int64_t s = 0; s < n; s++) {
+    const double x = points[2 * s] / h, y = points[2 * s + 1] / h;
+    if (!(x >= 0 && y >= 0 && x < nx && y < ny)) { free(P); return 2; }
+    if (mask[(size_t)(int)floor(y) * nx + (int)floor(x)]) { free(P); return 2; }
+  }
+  const size_t ne = (size_t)nx * ny * P->R.d;
+  int bad = 0;
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 1) reduction(| : bad)
+#endif
+  for (int64_t s = 0; s < n; s++) {
+    double *buf = (double *)malloc(sizeof(double) * 6 * ne);
+    double *u = buf;
+    const double x = points[2 * s] / h, y = points[2 * s + 1] / h;
+    const int is = (int)floor(x), js = (int)floor(y);
+    q_project_point(P, is, js, x - is, y - js, u);
+    for (int64_t k = 0; k < nsteps; k++)
+      q_ssprk3_step(P, u, buf + ne, buf + 2 * ne, buf + 3 * ne, buf + 4 * ne, dt);
+    double m[6];
+    q_moments_about(P, u, points[2 * s], points[2 * s + 1], m);
     for (int k = 0; k < 6; k++) {
       mom_out[s * 6 + k] = m[k];
       if (!isfinite(m[k])) bad |= 1;

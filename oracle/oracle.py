@@ -56,6 +56,8 @@ def lib():
         L.orc_q_apply_L.argtypes = [c_int, c_double, c_double, c_int, c_int, _u8p, _dp, _dp]
         L.orc_q_solve.argtypes = [c_int, c_double, c_double, c_int, c_int, _u8p, _i32p, c_i64, c_double, c_i64,
                                   _dp, _dp, c_int]
+        L.orc_q_solve_points.argtypes = [c_int, c_double, c_double, c_int, c_int, _u8p, _dp, c_i64, c_double,
+                                         c_i64, _dp, _dp, c_int]
         L.orc_solve_points.argtypes = [c_int, c_double, c_double, c_int, c_int, _u8p, c_int, _dp, c_i64,
                                        c_double, c_i64, _dp, _dp, c_int]
         L.orc_mixture.argtypes = [c_int, c_int, c_int, _dp, _i32p, _dp, c_i64, c_int, _dp]
@@ -64,7 +66,7 @@ def lib():
         L.orc_l2_err_gaussian.argtypes = [c_int, c_double, c_int, c_int, _dp, c_double, c_double, c_double, _dp]
         for f in (L.orc_reference, L.orc_basis, L.orc_apply_L, L.orc_advance, L.orc_moments,
                   L.orc_project_delta, L.orc_solve, L.orc_solve_points, L.orc_sigma, L.orc_q_reference,
-                  L.orc_q_apply_L, L.orc_q_solve, L.orc_project_gaussian, L.orc_l2_err_gaussian, L.orc_mixture, L.orc_residual):
+                  L.orc_q_apply_L, L.orc_q_solve, L.orc_q_solve_points, L.orc_project_gaussian, L.orc_l2_err_gaussian, L.orc_mixture, L.orc_residual):
             f.restype = c_int
         _lib = L
     return _lib
@@ -199,6 +201,19 @@ def q_solve(p, h, D, mask, sources, dt, nsteps, keep_density=False, nthreads=0):
     dens = np.zeros((n, ny, nx, qdof(p))) if keep_density else None
     _chk(lib().orc_q_solve(p, h, D, nx, ny, _p(mask, _u8p), _p(src, _i32p), n, dt, nsteps, _p(mom), _p(dens),
                            nthreads), "orc_q_solve")
+    return (mom, dens) if keep_density else mom
+
+
+def q_solve_points(p, h, D, mask, points, dt, nsteps, keep_density=False, nthreads=0):
+    """Quads (N4) with physical point sources (reading R21)."""
+    mask = _mask(mask)
+    ny, nx = mask.shape
+    pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 2)
+    n = pts.shape[0]
+    mom = np.zeros((n, 6))
+    dens = np.zeros((n, ny, nx, qdof(p))) if keep_density else None
+    _chk(lib().orc_q_solve_points(p, h, D, nx, ny, _p(mask, _u8p), _p(pts), n, dt, nsteps, _p(mom), _p(dens),
+                                  nthreads), "orc_q_solve_points")
     return (mom, dens) if keep_density else mom
 
 

@@ -412,6 +412,7 @@ struct dgdiff_s {
   void *d_A = nullptr;
   void *d_Aabs = nullptr;  // ABSORB boundary-pixel blocks (state precision)
   dgop::Table tab;
+  dgop::QuadTable qtab;      // N4 quads (element = 1)
   // chunk buffers
   void *d_U[3] = {nullptr, nullptr, nullptr};
   void *d_Ubase = nullptr;
@@ -620,7 +621,7 @@ static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
     H->own_stream = true;
   }
   // K0 operator tables
-  dgop::QuadTable qt;
+  dgop::QuadTable &qt = H->qtab;
   try {
     if (H->quad) qt = dgop::build_quad(H->p);
     else H->tab = dgop::build(H->p);
@@ -1380,7 +1381,6 @@ extern "C" dgdiff_status dgdiff_solve_batch_points(dgdiff_t H, const double *poi
                                                    int64_t nsteps) {
   if (!H) return fail(DGDIFF_E_ARG, "handle is NULL");
   if (n < 1 || !points) return fail(DGDIFF_E_ARG, "need n >= 1 points");
-  if (H->quad) return fail(DGDIFF_E_ARG, "sub-pixel points are implemented for the triangle elements only");
   if (n >= (1LL << 31)) return fail(DGDIFF_E_ARG, "too many sources");
   const int PXS = 2 + H->D2;
   std::vector<int32_t> pix((size_t)2 * n);
@@ -1396,7 +1396,8 @@ extern "C" dgdiff_status dgdiff_solve_batch_points(dgdiff_t H, const double *poi
     double *r = &px[(size_t)s * PXS];
     r[0] = x;
     r[1] = y;
-    dgop::point_init(H->tab, x - i, y - j, r + 2);
+    if (H->quad) dgop::point_init_quad(H->qtab, x - i, y - j, r + 2);
+    else dgop::point_init(H->tab, x - i, y - j, r + 2);
     const double ih2 = 1.0 / (H->h * H->h);
     for (int k = 0; k < H->D2; k++) r[2 + k] *= ih2;
   }

@@ -521,7 +521,32 @@ QuadTable build_quad(int p) {
     T.init[i] = s.to_double();
     T.cw[i] = peval(phi[i], Q(1, 2), Q(1, 2)).to_double();
   }
+  T.minv.assign((size_t)d * d, 0.0);
+  T.phic.assign((size_t)d * (p + 1) * (p + 1), 0.0);
+  for (int i = 0; i < d; i++) {
+    for (int j = 0; j < d; j++) T.minv[(size_t)i * d + j] = Mi[i][j].to_double();
+    for (int a = 0; a <= p; a++)
+      for (int b = 0; b <= p; b++) T.phic[((size_t)i * (p + 1) + a) * (p + 1) + b] = phi[i][a][b].to_double();
+  }
   return T;
+}
+
+void point_init_quad(const QuadTable &T, double xi, double eta, double *out) {
+  const int p = T.p, d = T.d;
+  double phi[16];
+  for (int k = 0; k < d; k++) {
+    double s = 0.0, xa = 1.0;
+    for (int a = 0; a <= p; a++, xa *= xi) {
+      double yb = 1.0;
+      for (int b = 0; b <= p; b++, yb *= eta) s += T.phic[((size_t)k * (p + 1) + a) * (p + 1) + b] * xa * yb;
+    }
+    phi[k] = s;
+  }
+  for (int i = 0; i < d; i++) {
+    double s = 0.0;
+    for (int j = 0; j < d; j++) s += T.minv[(size_t)i * d + j] * phi[j];
+    out[i] = s;
+  }
 }
 
 void point_init(const Table &T, double xi, double eta, double *out) {

@@ -40,8 +40,12 @@ struct QuadTable {
   std::vector<double> W;       // [6][d] moment weights on the unit pixel
   std::vector<double> init;    // [d] projected central Dirac, units 1/h^2
   std::vector<double> cw;      // [d] N_k(1/2, 1/2)
+  std::vector<double> minv;    // [d][d] M^-1 on the unit pixel
+  std::vector<double> phic;    // [d][p+1][p+1] coefficients of xi^a eta^b in N_k
 };
 QuadTable build_quad(int p);
+// projected Dirac at the pixel-local point (xi, eta): u = M^-1 N(xi, eta), out[d]
+void point_init_quad(const QuadTable &T, double xi, double eta, double *out);
 
 // Composite blocks of pixels with absorbing outer faces (outer_bc = ABSORB,
 // Eq. (4)): A[code][outer][5][2d][2d] (outer = faces on the outer square; zero

@@ -595,8 +595,9 @@ def test_p3_random_masks_and_free_space(dg, orc, prec):
     assert np.abs(S - 2.0 * np.eye(2)).max() <= (1e-11 if prec == 64 else 2e-4)
 
 
-@pytest.mark.parametrize("p,prec,windows", [(1, 64, 0), (1, 32, 0), (2, 64, 0), (1, 64, 1), (3, 64, 0)])
-def test_subpixel_points_vs_oracle(dg, orc, p, prec, windows):
+@pytest.mark.parametrize("p,prec,windows,element", [(1, 64, 0, 0), (1, 32, 0, 0), (2, 64, 0, 0), (1, 64, 1, 0),
+                                                    (3, 64, 0, 0), (1, 64, 0, 1), (2, 64, 1, 1), (2, 32, 0, 1)])
+def test_subpixel_points_vs_oracle(dg, orc, p, prec, windows, element):
     """N4 sub-pixel sources: points inside L, inside U, on the diagonal and on
     pixel edges (R21), a ragged two-chunk batch, against O1's solve_points
     (densities of the kept chunk, per-source moments about the point, Sigma)."""
@@ -604,7 +605,7 @@ def test_subpixel_points_vs_oracle(dg, orc, p, prec, windows):
     ny, nx = 22, 26
     m = (rng.random((ny, nx)) < 0.35).astype(np.uint8)
     free = np.argwhere(m == 0)
-    G = {1: 64, 2: 32, 3: 32}[p] * (2 if prec == 32 else 1)
+    G = ({1: 64, 2: 32, 3: 32}[p] if element == 0 else 32) * (2 if prec == 32 else 1)
     n = G + 9
     pick = free[rng.integers(0, len(free), n)]
     loc = rng.random((n, 2))
@@ -614,9 +615,11 @@ def test_subpixel_points_vs_oracle(dg, orc, p, prec, windows):
     loc[3] = (0.5, 0.5)        # centre
     h = 0.8
     pts = (np.stack([pick[:, 1], pick[:, 0]], 1) + loc) * h
-    dt = {1: 1 / 32, 2: 1 / 128, 3: 1 / 256}[p] * h * h / 1.3
-    ref_m, ref_d = orc.solve_points(p, h, 1.3, m, pts, dt, 30, keep_density=True)
-    with dg.Solver(m, h, 1.3, p, precision=prec, keep_density=1, max_chunk=G, windows=windows) as s:
+    dt = ({1: 1 / 32, 2: 1 / 128, 3: 1 / 256} if element == 0 else {1: 1 / 16, 2: 1 / 64})[p] * h * h / 1.3
+    osolve = orc.solve_points if element == 0 else orc.q_solve_points
+    ref_m, ref_d = osolve(p, h, 1.3, m, pts, dt, 30, keep_density=True)
+    with dg.Solver(m, h, 1.3, p, precision=prec, keep_density=1, max_chunk=G, windows=windows,
+                   element=element) as s:
         s.solve_points(pts, dt, 30)
         S, mu = s.covariance()
         mom = s.moments()

@@ -635,3 +635,25 @@ def test_quad_spectral_radius_pins_dt_max(orc, p, rho):
         assert lam.real.max() < 1e-9
         seen = max(seen, np.abs(lam).max())
     assert seen <= rho and rho <= 1.01 * seen, seen
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_quad_points(orc, p):
+    """Quads with sub-pixel points (R21): a centre point is the pixel source
+    (bitwise); the projection reproduces the moments the tensor space holds
+    (mass 1 and first moments 0 for Q1 and Q2; second moments 0 for Q2);
+    whole-pixel translation in free space changes no moment."""
+    mask, src = _case(51)
+    pts = [(i + 0.5, j + 0.5) for i, j in src]
+    assert np.array_equal(orc.q_solve_points(p, 1.0, 1.0, mask, pts, 1 / 64, 10), orc.q_solve(p, 1.0, 1.0, mask, src, 1 / 64, 10))
+    m = np.zeros((6, 6), np.uint8)
+    h = 0.7
+    P0 = [(2.71 * h, 3.22 * h), (2.0 * h, 3.3 * h), (2.6 * h, 3.0 * h)]
+    mom = orc.q_solve_points(p, h, 1.0, m, P0, 1e-3, 0)
+    assert np.allclose(mom[:, 0], 1.0, rtol=0, atol=1e-13)
+    assert np.abs(mom[:, 1:3]).max() <= 1e-13
+    if p == 2:
+        assert np.abs(mom[:, 3:]).max() <= 1e-13
+    f = np.zeros((96, 96), np.uint8)                   # walls >= 45 sigma (Q2 tails are long)
+    a = orc.q_solve_points(p, 1.0, 1.0, f, [(47.3, 48.6), (48.3, 48.6)], 1 / 64, 32)
+    assert np.allclose(a[0], a[1], rtol=0, atol=1e-12)
