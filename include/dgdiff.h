@@ -78,7 +78,8 @@ typedef struct {
                              by bulk TMA.  Results agree to rounding; the
                              state layout (and so the source-group size) differs:
                              v1/v2 16-byte lanes; v3 16-byte lanes for P1,
-                             8-byte lanes for P2 */
+                             8-byte lanes for P2, P3 and the quadrilaterals.
+                             v1/v2 exist for the P1/P2 triangles only */
   int32_t mixture_radius; /* R > 0: accumulate the mixture density grid
                              on the displacement lattice [-R, R]^2 (pixel
                              units) during dgdiff_solve_batch, for
@@ -197,13 +198,16 @@ dgdiff_status dgdiff_source_moments(dgdiff_t, double *out);
 
 /* Final state of source `src` of the last solve, in the canonical fp64 layout
  * [ny][nx][2][d] (triangle 0 = L (0,0),(1,0),(1,1); 1 = U (0,0),(1,1),(0,1);
- * nodes: vertices, then edge nodes of v0v1, v1v2, v2v0, then interior).
+ * nodes: vertices, then edge nodes of v0v1, v1v2, v2v0, then interior);
+ * quadrilaterals: [ny][nx][(p+1)^2], dof b (p+1) + a at the node (a/p, b/p).
  * Requires keep_density and src in this rank's last chunk -> else E_STATE. */
 dgdiff_status dgdiff_get_density(dgdiff_t, int64_t src, double *out);
 
-/* Largest stable SSP-RK3 step: 2.5127453 / rho_p * h^2 / D with the Bloch
- * spectral radius rho_1 = 60, rho_2 = 192.7953 (reading R8);
- * 0 for an unsupported degree. */
+/* Largest stable SSP-RK3 step for the triangle elements: 2.5127453 / rho_p *
+ * h^2 / D with rho_1 = 60, rho_2 = 192.7953, rho_3 = 462.37 (DESIGN.md
+ * reading R8; pinned against the assembled operator's spectrum); 0 for an
+ * unsupported degree.  The quadrilaterals use rho_Q1 = 32, rho_Q2 = 130.7
+ * (R22) inside dgdiff_solve_batch. */
 double dgdiff_dt_max(int32_t degree, double h, double D);
 
 /* Thread-local message of the last failing call ("" if none). */
