@@ -81,8 +81,9 @@ def local(p, h):
     return M, D, faces
 
 
-def assemble(p, h, Dif, mask):
-    """Dense L (REFLECT) on the grid mask [ny][nx], dof order [j][i][k]."""
+def assemble(p, h, Dif, mask, outer_bc=0):
+    """Dense L on the grid mask [ny][nx], dof order [j][i][k]; outer_bc 0 =
+    REFLECT (outside = axon), 1 = ABSORB (Eq. (4): h_u = 0, h_q = k q- . n)."""
     ny, nx = mask.shape
     d = qdof(p)
     M, D, faces = local(p, h)
@@ -104,6 +105,10 @@ def assemble(p, h, Dif, mask):
             for Em, Ep, (di, dj), nrm in faces:
                 ii, jj = i + di, j + dj
                 inside = 0 <= ii < nx and 0 <= jj < ny
+                if not inside and outer_bc == 1:
+                    for c in range(2):
+                        B[c][K, K] += k[j, i] * nrm[c] * Em
+                    continue
                 for c in range(2):
                     G[c][K, K] += 0.5 * nrm[c] * Em
                     if inside:

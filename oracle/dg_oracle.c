@@ -963,6 +963,7 @@ typedef struct {
   qref_t R;
   int nx, ny;
   double D;
+  int outer_bc;   /* 0 = REFLECT (R9), 1 = ABSORB = Eq. (4): ghost u+ = -u-, q+ = q-, k+ = k- */
   const uint8_t *mask;
 } qprob_t;
 
@@ -993,6 +994,7 @@ static void q_apply_L(const qprob_t *P, const double *u, double *q, double *Lu) 
       for (int f = 0; f < 4; f++) {
         const int in = i + QNB[f][0], jn = j + QNB[f][1];
         const int outside = (in < 0 || jn < 0 || in >= nx || jn >= ny);
+        if (outside && P->outer_bc == 1) continue;   /* ABSORB: h_u = (u- + u+)/2 = 0 */
         const double *un = outside ? zero : u + qidx(P, in, jn);   /* u+ = 0 outside (R6, R9) */
         for (int a = 0; a < d; a++) {
           double s = 0.0;
@@ -1025,6 +1027,16 @@ static void q_apply_L(const qprob_t *P, const double *u, double *q, double *Lu) 
       }
       for (int f = 0; f < 4; f++) {
         const int in = i + QNB[f][0], jn = j + QNB[f][1];
+        if ((in < 0 || jn < 0 || in >= nx || jn >= ny) && P->outer_bc == 1) {
+          /* ABSORB: q+ = q-, k+ = k-  =>  h_q = k_K q- . n */
+          for (int a = 0; a < d; a++) {
+            double sc = 0.0;
+            for (int c = 0; c < 2; c++)
+              for (int b = 0; b < d; b++) sc += QNRM[f][c] * R->Em[f][a][b] * qK[c][b];
+            r[a] += kK * sc;
+          }
+          continue;
+        }
         const double kf = harmonic(kK, qkpix(P, in, jn));
         if (kf == 0.0) continue;
         const double *qN[2] = {qx + qidx(P, in, jn), qy + qidx(P, in, jn)};
@@ -1117,12 +1129,13 @@ static void q_moments_about(const qprob_t *P, const double *u, double xs, double
     }
 }
 
-static int q_setup(qprob_t *P, int p, double h, double D, int nx, int ny, const uint8_t *mask) {
-  if (p < 1 || p > 3 || !(h > 0) || !(D > 0) || nx < 1 || ny < 1 || !mask) return 1;
+static int q_setup(qprob_t *P, int p, double h, double D, int nx, int ny, const uint8_t *mask, int outer_bc) {
+  if (p < 1 || p > 3 || !(h > 0) || !(D > 0) || nx < 1 || ny < 1 || !mask || outer_bc < 0 || outer_bc > 1) return 1;
   qref_init(&P->R, p, h);
   P->nx = nx;
   P->ny = ny;
   P->D = D;
+  P->outer_bc = outer_bc;
   P->mask = mask;
   return 0;
 }
@@ -1148,9 +1161,10 @@ int orc_q_reference(int p, double h, double *M, double *Minv, double *Dc, double
 }
 
 /* u, out: [ny][nx][(p+1)^2] */
-int orc_q_apply_L(int p, double h, double D, int nx, int ny, const uint8_t *mask, const double *u, double *out) {
+int orc_q_apply_L(int p, double h, double D, int nx, int ny, const uint8_t *mask, int outer_bc, const double *u,
+                  double *out) {
   qprob_t *P = (qprob_t *)malloc(sizeof(qprob_t));
-  if (q_setup(P, p, h, D, nx, ny, mask)) { free(P); return 1; }
+  if (q_setup(P, p, h, D, nx, ny, mask, outer_bc)) { free(P); return 1; }
   double *q = (double *)malloc(sizeof(double) * 2 * (size_t)nx * ny * P->R.d);
   q_apply_L(P, u, q, out);
   free(q);
@@ -1158,11 +1172,11 @@ int orc_q_apply_L(int p, double h, double D, int nx, int ny, const uint8_t *mask
   return 0;
 }
 
-/* as orc_solve (REFLECT), for Q_p; dens_out: NULL or [n][ny][nx][(p+1)^2] */
-int orc_q_solve(int p, double h, double D, int nx, int ny, const uint8_t *mask, const int32_t *sources, int64_t n,
-                double dt, int64_t nsteps, double *mom_out, double *dens_out, int nthreads) {
+/* as orc_solve, for Q_p (REFLECT or ABSORB); dens_out: NULL or [n][ny][nx][(p+1)^2] */
+int orc_q_solve(int p, double h, double D, int nx, int ny, const uint8_t *mask, int outer_bc, const int32_t *sources,
+                int64_t n, double dt, int64_t nsteps, double *mom_out, double *dens_out, int nthreads) {
   qprob_t *P = (qprob_t *)malloc(sizeof(qprob_t));
-  if (q_setup(P, p, h, D, nx, ny, mask) || n < 0 || nsteps < 0 || !(dt >= 0)) { free(P); return 1; }
+  if (q_setup(P, p, h, D, nx, ny, mask, outer_bc) || n < 0 || nsteps < 0 || !(dt >= 0)) { free(P); return 1; }
   for (int64_t s = 0; s < n; s++) {
     int is = sources[2 * s], js = sources[2 * s + 1];
     if (is < 0 || js < 0 || is >= nx || js >= ny || mask[(size_t)js * nx + is]) { free(P); return 2; }
@@ -1198,7 +1212,7 @@ int orc_q_solve(int p, double h, double D, int nx, int ny, const uint8_t *mask, 
 int orc_q_solve_points(int p, double h, double D, int nx, int ny, const uint8_t *mask, const double *points,
                        int64_t n, double dt, int64_t nsteps, double *mom_out, double *dens_out, int nthreads) {
   qprob_t *P = (qprob_t *)malloc(sizeof(qprob_t));
-  if (q_setup(P, p, h, D, nx, ny, mask) || n < 0 || nsteps < 0 || !(dt >= 0)) { free(P); return 1; }
+  if (q_setup(P, p, h, D, nx, ny, mask, 0) || n < 0 || nsteps < 0 || !(dt >= 0)) { free(P); return 1; }
   for (int64_t s = 0; s < n; s++) {
     const double x = points[2 * s] / h, y = points[2 * s + 1] / h;
     if (!(x >= 0 && y >= 0 && x < nx && y < ny)) { free(P); return 2; }

@@ -53,9 +53,9 @@ def lib():
                                 c_double, c_i64, _dp, _dp, c_int]
         L.orc_sigma.argtypes = [_dp, c_i64, c_int, _dp, _dp]
         L.orc_q_reference.argtypes = [c_int, c_double] + [_dp] * 5
-        L.orc_q_apply_L.argtypes = [c_int, c_double, c_double, c_int, c_int, _u8p, _dp, _dp]
-        L.orc_q_solve.argtypes = [c_int, c_double, c_double, c_int, c_int, _u8p, _i32p, c_i64, c_double, c_i64,
-                                  _dp, _dp, c_int]
+        L.orc_q_apply_L.argtypes = [c_int, c_double, c_double, c_int, c_int, _u8p, c_int, _dp, _dp]
+        L.orc_q_solve.argtypes = [c_int, c_double, c_double, c_int, c_int, _u8p, c_int, _i32p, c_i64, c_double,
+                                  c_i64, _dp, _dp, c_int]
         L.orc_q_solve_points.argtypes = [c_int, c_double, c_double, c_int, c_int, _u8p, _dp, c_i64, c_double,
                                          c_i64, _dp, _dp, c_int]
         L.orc_solve_points.argtypes = [c_int, c_double, c_double, c_int, c_int, _u8p, c_int, _dp, c_i64,
@@ -183,24 +183,24 @@ def q_reference(p, h=1.0) -> dict:
     return out
 
 
-def q_apply_L(p, h, D, mask, u) -> np.ndarray:
+def q_apply_L(p, h, D, mask, u, outer_bc=REFLECT) -> np.ndarray:
     mask = _mask(mask)
     ny, nx = mask.shape
     u = np.ascontiguousarray(u, dtype=np.float64).reshape(ny, nx, qdof(p))
     out = np.zeros_like(u)
-    _chk(lib().orc_q_apply_L(p, h, D, nx, ny, _p(mask, _u8p), _p(u), _p(out)), "orc_q_apply_L")
+    _chk(lib().orc_q_apply_L(p, h, D, nx, ny, _p(mask, _u8p), outer_bc, _p(u), _p(out)), "orc_q_apply_L")
     return out
 
 
-def q_solve(p, h, D, mask, sources, dt, nsteps, keep_density=False, nthreads=0):
+def q_solve(p, h, D, mask, sources, dt, nsteps, keep_density=False, nthreads=0, outer_bc=REFLECT):
     mask = _mask(mask)
     ny, nx = mask.shape
     src = np.ascontiguousarray(sources, dtype=np.int32).reshape(-1, 2)
     n = src.shape[0]
     mom = np.zeros((n, 6))
     dens = np.zeros((n, ny, nx, qdof(p))) if keep_density else None
-    _chk(lib().orc_q_solve(p, h, D, nx, ny, _p(mask, _u8p), _p(src, _i32p), n, dt, nsteps, _p(mom), _p(dens),
-                           nthreads), "orc_q_solve")
+    _chk(lib().orc_q_solve(p, h, D, nx, ny, _p(mask, _u8p), outer_bc, _p(src, _i32p), n, dt, nsteps, _p(mom),
+                           _p(dens), nthreads), "orc_q_solve")
     return (mom, dens) if keep_density else mom
 
 

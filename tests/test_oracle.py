@@ -657,3 +657,23 @@ def test_quad_points(orc, p):
     f = np.zeros((96, 96), np.uint8)                   # walls >= 45 sigma (Q2 tails are long)
     a = orc.q_solve_points(p, 1.0, 1.0, f, [(47.3, 48.6), (48.3, 48.6)], 1 / 64, 32)
     assert np.allclose(a[0], a[1], rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_quad_absorb_matches_dense_and_loses_mass(orc, p):
+    """Quads under ABSORB (Eq. (4): h_u = 0 and h_q = k q- . n on the outer
+    square): O1q == O2q on random masks touching every edge, and mass leaves
+    through the outer square (it is conserved under REFLECT)."""
+    from oracle import dense_quad as Q
+    rng = np.random.default_rng(90 + p)
+    d = (p + 1) ** 2
+    mask = (rng.random((6, 7)) < 0.3).astype(np.uint8)
+    u = rng.standard_normal((6, 7, d))
+    u[mask.astype(bool)] = 0
+    ref = (Q.assemble(p, 0.7, 1.3, mask, 1) @ u.reshape(-1)).reshape(u.shape)
+    got = orc.q_apply_L(p, 0.7, 1.3, mask, u, outer_bc=1)
+    assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
+    m = np.zeros((10, 10), np.uint8)
+    mr = orc.q_solve(p, 1.0, 1.0, m, [(1, 1)], 1 / 64, 100)
+    ma = orc.q_solve(p, 1.0, 1.0, m, [(1, 1)], 1 / 64, 100, outer_bc=1)
+    assert abs(mr[0, 0] - 1) < 1e-13 and ma[0, 0] < 0.9
