@@ -55,7 +55,7 @@ typedef struct {
                              (P:67-70): u = 0 on the outer square (ghost u+ = -u-);
                              mass leaves the grid.  ABSORB runs on the default
                              ring kernel only (kernel 1/2 or temporal_steps 2 ->
-                             E_ARG) */
+                             E_ARG), for P1/P2 triangles and Q1/Q2 quads */
   int32_t centering;      /* 0 = shift each density by its source point (default,
                              reading R12); 1 = by its own mean */
   int32_t temporal_steps; /* 0 = library choice; 1 = one launch per RK stage
@@ -108,8 +108,8 @@ typedef struct {
                              star's "Q2"; degree 1 or 2): tensor Lagrange basis
                              on (a/p, b/p), dof b (p+1) + a, same fluxes; the
                              composite operator is a 9-point cross.  Default
-                             ring kernel and REFLECT only; densities are
-                             [ny][nx][(p+1)^2] */
+                             ring kernel only (REFLECT or ABSORB); densities
+                             are [ny][nx][(p+1)^2] */
 } dgdiff_opts;
 
 /* Fill *o with the defaults above. */

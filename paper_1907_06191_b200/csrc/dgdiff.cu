@@ -822,7 +822,7 @@ static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
   if (H->o.outer_bc == 1) {
     std::vector<double> Ab;
     try {
-      Ab = dgop::build_absorb(H->p);
+      Ab = H->quad ? dgop::build_quad_absorb(H->p) : dgop::build_absorb(H->p);
     } catch (std::exception &ex) {
       return fail(DGDIFF_E_ARG, "absorbing operator precompute failed: %s", ex.what());
     }
@@ -910,8 +910,8 @@ extern "C" dgdiff_status dgdiff_create(dgdiff_t *out, const uint8_t *mask, int32
     return fail(DGDIFF_E_ARG, "windows (N1) run on the default ring kernel only");
   if (o.centering != 0 && o.centering != 1) return fail(DGDIFF_E_ARG, "centering must be 0 or 1");
   if (o.element != 0 && o.element != 1) return fail(DGDIFF_E_ARG, "element must be 0 (triangles) or 1 (quadrilaterals)");
-  if (o.element == 1 && (degree > 2 || o.kernel == 1 || o.kernel == 2 || o.temporal_steps == 2 || o.outer_bc != 0))
-    return fail(DGDIFF_E_ARG, "quadrilateral Q_p (N4): degree 1 or 2, default ring kernel, REFLECT only");
+  if (o.element == 1 && (degree > 2 || o.kernel == 1 || o.kernel == 2 || o.temporal_steps == 2))
+    return fail(DGDIFF_E_ARG, "quadrilateral Q_p (N4): degree 1 or 2, default ring kernel only");
   if (o.nranks < 1 || o.rank < 0 || o.rank >= o.nranks) return fail(DGDIFF_E_ARG, "bad rank/nranks");
   if (o.temporal_steps < 0) return fail(DGDIFF_E_ARG, "temporal_steps < 0");
   if (o.max_chunk < 0) return fail(DGDIFF_E_ARG, "max_chunk < 0");

@@ -394,6 +394,9 @@ Table build(int p) {
 }
 
 // ---- N4: quadrilateral Q_p elements ----------------------------------------
+struct QuadRef;
+static void quad_ref(int p, QuadRef &R);
+
 QuadTable build_quad(int p) {
   if (p < 1 || p > 2) throw std::runtime_error("quadrilateral elements: degree must be 1 or 2");
   const int d = (p + 1) * (p + 1);
@@ -527,6 +530,133 @@ QuadTable build_quad(int p) {
     for (int j = 0; j < d; j++) T.minv[(size_t)i * d + j] = Mi[i][j].to_double();
     for (int a = 0; a <= p; a++)
       for (int b = 0; b <= p; b++) T.phic[((size_t)i * (p + 1) + a) * (p + 1) + b] = phi[i][a][b].to_double();
+  }
+  return T;
+}
+
+// ---- quads under ABSORB (Eq. (4)) ----------------------------------------------
+// outer faces: h_u = 0 (no u-flux term at all) and h_q = k q- . n (full, not
+// halved).  Layout: self [16 code][16 outer][d][d], then N [4 f][3 opposite
+// state: 0 closed, 1 open, 2 outer][2 far face outer][d][d], then NN [4][d][d].
+struct QuadRef {
+  int d = 0;
+  Mat Mi, Dc[2], Em[4], Ep[4];
+};
+
+static void quad_ref(int p, QuadRef &R) {
+  const int d = (p + 1) * (p + 1);
+  std::vector<std::pair<int, int>> mons;
+  for (int b = 0; b <= p; b++)
+    for (int a = 0; a <= p; a++) mons.push_back({a, b});
+  Mat V = zeros(d, d);
+  for (int n = 0; n < d; n++)
+    for (int m = 0; m < d; m++)
+      V[n][m] = qpow(Q(mons[n].first, p), mons[m].first) * qpow(Q(mons[n].second, p), mons[m].second);
+  Mat C = inverse(V);
+  std::vector<Poly2> phi(d, Poly2(p + 1, std::vector<Q>(p + 1, Q(0))));
+  for (int k = 0; k < d; k++)
+    for (int m = 0; m < d; m++) phi[k][mons[m].first][mons[m].second] = C[m][k];
+  auto sq = [&](const Poly2 &P) {
+    Q s(0);
+    for (size_t a = 0; a < P.size(); a++)
+      for (size_t b = 0; b < P[a].size(); b++)
+        if (!P[a][b].zero()) s += P[a][b] * Q(1, (i128)(a + 1) * (i128)(b + 1));
+    return s;
+  };
+  Mat M = zeros(d, d);
+  R.Dc[0] = zeros(d, d);
+  R.Dc[1] = zeros(d, d);
+  for (int i = 0; i < d; i++)
+    for (int j = 0; j < d; j++) {
+      M[i][j] = sq(pmul(phi[i], phi[j]));
+      for (int c = 0; c < 2; c++) R.Dc[c][i][j] = sq(pmul(pderiv(phi[i], c), phi[j]));
+    }
+  R.Mi = inverse(M);
+  const int FA[4][2] = {{1, 0}, {0, 0}, {0, 1}, {0, 0}}, FB[4][2] = {{1, 1}, {0, 1}, {1, 1}, {1, 0}};
+  const int OFF[4][2] = {{1, 0}, {-1, 0}, {0, 1}, {0, -1}};
+  for (int f = 0; f < 4; f++) {
+    R.Em[f] = zeros(d, d);
+    R.Ep[f] = zeros(d, d);
+    Q x0(FA[f][0]), y0(FA[f][1]), dx(FB[f][0] - FA[f][0]), dy(FB[f][1] - FA[f][1]);
+    std::vector<Poly1> pm(d), pn(d);
+    for (int i = 0; i < d; i++) {
+      pm[i] = restrict_line(phi[i], x0, dx, y0, dy);
+      pn[i] = restrict_line(phi[i], x0 - Q(OFF[f][0]), dx, y0 - Q(OFF[f][1]), dy);
+    }
+    for (int i = 0; i < d; i++)
+      for (int j = 0; j < d; j++) {
+        R.Em[f][i][j] = integrate1(p1mul(pm[i], pm[j]));
+        R.Ep[f][i][j] = integrate1(p1mul(pm[i], pn[j]));
+      }
+  }
+  R.d = d;
+}
+
+std::vector<double> build_quad_absorb(int p) {
+  if (p < 1 || p > 2) throw std::runtime_error("quadrilateral elements: degree must be 1 or 2");
+  QuadRef R;
+  quad_ref(p, R);
+  const int d = R.d, NRM[4][2] = {{1, 0}, {-1, 0}, {0, 1}, {0, -1}}, OPP[4] = {1, 0, 3, 2};
+  // q of an element with outer face set `out`: S0 (own u) and P_f (across face f)
+  auto S0 = [&](int out, int c) {
+    Mat t = zeros(d, d);
+    axpy(t, Q(-1), R.Dc[c]);
+    for (int f = 0; f < 4; f++)
+      if (!((out >> f) & 1) && NRM[f][c]) axpy(t, Q(NRM[f][c], 2), R.Em[f]);
+    return mul(R.Mi, t);
+  };
+  auto Pf = [&](int f, int c) {
+    Mat e = zeros(d, d);
+    if (NRM[f][c]) axpy(e, Q(NRM[f][c], 2), R.Ep[f]);
+    return mul(R.Mi, e);
+  };
+  auto Tc = [&](int code, int out, int c) {
+    Mat t = zeros(d, d);
+    axpy(t, Q(-1), R.Dc[c]);
+    for (int f = 0; f < 4; f++) {
+      if (!NRM[f][c]) continue;
+      if ((code >> f) & 1) axpy(t, Q(NRM[f][c], 2), R.Em[f]);
+      if ((out >> f) & 1) axpy(t, Q(NRM[f][c]), R.Em[f]);   // ABSORB q-flux: k q- . n
+    }
+    return t;
+  };
+  std::vector<double> T((size_t)(256 + 24 + 4) * d * d, 0.0);
+  auto put = [&](size_t b, const Mat &A) {
+    for (int i = 0; i < d; i++)
+      for (int j = 0; j < d; j++) T[(b * d + i) * d + j] = A[i][j].to_double();
+  };
+  for (int code = 0; code < 16; code++)
+    for (int out = 0; out < 16; out++) {
+      if (code & out) continue;
+      Mat A = zeros(d, d);
+      for (int c = 0; c < 2; c++) {
+        Mat t = mul(Tc(code, out, c), S0(out, c));
+        for (int f = 0; f < 4; f++)
+          if (((code >> f) & 1) && NRM[f][c]) axpy(t, Q(NRM[f][c], 2), mul(R.Ep[f], Pf(OPP[f], c)));
+        for (int i = 0; i < d; i++)
+          for (int j = 0; j < d; j++) A[i][j] += t[i][j];
+      }
+      put((size_t)code * 16 + out, mul(R.Mi, A));
+    }
+  for (int f = 0; f < 4; f++)
+    for (int os = 0; os < 3; os++)
+      for (int far = 0; far < 2; far++) {
+        const int code = (1 << f) | (os == 1 ? 1 << OPP[f] : 0), out = os == 2 ? 1 << OPP[f] : 0;
+        const int nout = far ? 1 << f : 0;   // the neighbour's far face on the outer square
+        Mat A = zeros(d, d);
+        for (int c = 0; c < 2; c++) {
+          Mat t = mul(Tc(code, out, c), Pf(f, c));
+          if (NRM[f][c]) axpy(t, Q(NRM[f][c], 2), mul(R.Ep[f], S0(nout, c)));
+          for (int i = 0; i < d; i++)
+            for (int j = 0; j < d; j++) A[i][j] += t[i][j];
+        }
+        put(256 + ((size_t)f * 3 + os) * 2 + far, mul(R.Mi, A));
+      }
+  for (int f = 0; f < 4; f++) {
+    Mat A = zeros(d, d);
+    for (int c = 0; c < 2; c++)
+      if (NRM[f][c]) axpy(A, Q(NRM[f][c], 2), mul(R.Ep[f], Pf(f, c)));
+    put(280 + f, mul(R.Mi, A));
   }
   return T;
 }

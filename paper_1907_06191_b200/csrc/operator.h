@@ -44,6 +44,10 @@ struct QuadTable {
   std::vector<double> phic;    // [d][p+1][p+1] coefficients of xi^a eta^b in N_k
 };
 QuadTable build_quad(int p);
+// quads under ABSORB (Eq. (4)): self [16 code][16 outer][d][d], then N [4 f][3
+// opposite-face state: 0 closed, 1 open, 2 outer][2 far face outer][d][d],
+// then NN [4][d][d]; units D/h^2
+std::vector<double> build_quad_absorb(int p);
 // projected Dirac at the pixel-local point (xi, eta): u = M^-1 N(xi, eta), out[d]
 void point_init_quad(const QuadTable &T, double xi, double eta, double *out);
 

@@ -334,6 +334,33 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
         // steps on (when extracellular); the corners couple to nothing
         const int4 nb2 = nbr_ring[(size_t)sl2 * Gm::NBW + 1];
         const int code = open_code(nb);
+        const int far_out = (nb2.x == -2) | ((nb2.y == -2) << 1) | ((nb2.z == -2) << 2) | ((nb2.w == -2) << 3);
+        if (__builtin_expect((outer | far_out) != 0, 0)) {
+          // ABSORB within two pixels of the outer square: K0's runtime blocks
+          // (self by (code, outer); neighbour by (opposite-face state, far
+          // face outer); far block fixed), see build_quad_absorb
+          const T *Ab = Aabs;
+          mv_gen<T, NV, D2>(acc, Ab + (size_t)(code * 16 + outer) * D2 * D2, xs);
+          const int nbv[4] = {nb.x, nb.y, nb.z, nb.w}, far[4] = {nb2.x, nb2.y, nb2.z, nb2.w};
+#pragma unroll 1
+          for (int f = 0; f < 4; f++) {
+            if (nbv[f] < 0) continue;
+            const int o = f ^ 1;   // opposite face (E<->W, N<->S)
+            const int os = nbv[o] >= 0 ? 1 : (nbv[o] == -2 ? 2 : 0);
+            const RowMeta mf = f < 2 ? mc : meta[seq(f == 2 ? j + 1 : j - 1) % Q];
+            const T *pn = tile1(mf, nbv[f]);
+#pragma unroll
+            for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
+            mv_gen<T, NV, D2>(acc, Ab + (size_t)(256 + (f * 3 + os) * 2 + (far[f] == -2)) * D2 * D2, xn);
+            if (far[f] >= 0) {
+              const RowMeta mff = f < 2 ? mc : meta[seq(f == 2 ? j + 2 : j - 2) % Q];
+              const T *pf = tile1(mff, far[f]);
+#pragma unroll
+              for (int k = 0; k < D2; k++) lds<T, NV>(pf + k * G, xn[k]);
+              mv_gen<T, NV, D2>(acc, Ab + (size_t)(280 + f) * D2 * D2, xn);
+            }
+          }
+        } else {
         mv_self<T, NV, P>(code, acc, xs);
         if (nb.x >= 0) {
           const T *pn = tile1(mc, nb.x);
@@ -383,6 +410,7 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
             mv_imm<T, NV, P, 27>(acc, xn);
           }
         }
+        }   // interior / REFLECT quads
       } else if (__builtin_expect(outer == 0, 1)) {
         // self block of this pixel's open-face code (compile-time immediates),
         // then the fixed neighbour blocks of the open faces

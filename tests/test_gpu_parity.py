@@ -802,3 +802,33 @@ def test_windows_sigma_clip(dg, cfg, p, element):
     assert mom_err(res[2][0], res[0][0]) <= 1e-12
     assert np.abs(res[2][1] - res[0][1]).max() <= 1e-12 * res[0][1].max()
     assert res[2][2] < res[0][2]
+
+
+@pytest.mark.parametrize("p,prec,windows", [(1, 64, 0), (2, 64, 0), (2, 32, 0), (2, 64, 1)])
+def test_quads_absorb_vs_oracle(dg, orc, p, prec, windows):
+    """Quads under ABSORB (Eq. (4)): pixels within two of the outer square use
+    K0's runtime blocks (self by (code, outer), neighbour by opposite-face
+    state and far-face-outer); sources next to every edge, against O1q."""
+    rng = np.random.default_rng(800 + 10 * p + prec + windows)
+    ny, nx = 19, 23
+    m = (rng.random((ny, nx)) < 0.3).astype(np.uint8)
+    free = np.argwhere(m == 0)
+    edge = free[(free[:, 0] <= 1) | (free[:, 0] >= ny - 2) | (free[:, 1] <= 1) | (free[:, 1] >= nx - 2)]
+    G = 32 if prec == 64 else 64
+    pick = np.concatenate([edge[:G // 2], free[rng.integers(0, len(free), G // 2 + 5)]])
+    src = np.stack([pick[:, 1], pick[:, 0]], 1).astype(np.int32)
+    n = len(src)
+    dt = (1 / 16 if p == 1 else 1 / 64) * 0.64 / 1.2
+    ref_m, ref_d = orc.q_solve(p, 0.8, 1.2, m, src, dt, 40, keep_density=True, outer_bc=1)
+    with dg.Solver(m, 0.8, 1.2, p, precision=prec, keep_density=1, max_chunk=G, element=1, outer_bc=1,
+                   windows=windows) as s:
+        s.solve(src, dt, 40)
+        S, mu = s.covariance()
+        mom = s.moments()
+        dens = {k: s.density(k) for k in range(n) if _in_last_chunk(s, k)}
+    t = TOL[prec]
+    assert len(dens) > 0
+    for k, dk in dens.items():
+        assert rel_l2(dk, ref_d[k]) <= t["dens"], k
+    assert mom_err(mom, ref_m) <= t["mom"]
+    assert (ref_m[:, 0] < 1 - 1e-6).any()          # mass really leaves through the outer square
