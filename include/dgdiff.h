@@ -55,7 +55,7 @@ typedef struct {
                              (P:67-70): u = 0 on the outer square (ghost u+ = -u-);
                              mass leaves the grid.  ABSORB runs on the default
                              ring kernel only (kernel 1/2 or temporal_steps 2 ->
-                             E_ARG), for P1/P2 triangles and Q1/Q2 quads */
+                             E_ARG), for every element type */
   int32_t centering;      /* 0 = shift each density by its source point (default,
                              reading R12); 1 = by its own mean */
   int32_t temporal_steps; /* 0 = library choice; 1 = one launch per RK stage
@@ -120,7 +120,7 @@ void dgdiff_opts_default(dgdiff_opts *o);
  *         (k = D); copied.
  *  h, D   pixel side and extracellular diffusivity k0 (> 0).
  *  degree Lagrange degree p of the triangle elements (Eq. (8); "p <= 3
- *         suffices"): 1, 2 or 3 (P3: default ring kernel, REFLECT only; its
+ *         suffices"): 1, 2 or 3 (P3: default ring kernel only; its
  *         non-dyadic operator entries are rounded once to the state type).
  * Builds the operator tables (host), the open-face code of every pixel and the
  * active-pixel index, copies them to the device; when nranks > 1 initialises

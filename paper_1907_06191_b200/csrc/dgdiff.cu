@@ -904,8 +904,8 @@ extern "C" dgdiff_status dgdiff_create(dgdiff_t *out, const uint8_t *mask, int32
   if (o.outer_bc == 1 && (o.kernel == 1 || o.kernel == 2 || o.temporal_steps == 2))
     return fail(DGDIFF_E_ARG, "outer_bc ABSORB runs on the default ring kernel only");
   if (o.windows < 0 || o.windows > 2) return fail(DGDIFF_E_ARG, "windows must be 0, 1 or 2");
-  if (degree == 3 && (o.kernel == 1 || o.kernel == 2 || o.temporal_steps == 2 || o.outer_bc != 0))
-    return fail(DGDIFF_E_ARG, "P3 (N4) runs on the default ring kernel with REFLECT only");
+  if (degree == 3 && (o.kernel == 1 || o.kernel == 2 || o.temporal_steps == 2))
+    return fail(DGDIFF_E_ARG, "P3 (N4) runs on the default ring kernel only");
   if (o.windows != 0 && (o.kernel == 1 || o.kernel == 2 || o.temporal_steps == 2))
     return fail(DGDIFF_E_ARG, "windows (N1) run on the default ring kernel only");
   if (o.centering != 0 && o.centering != 1) return fail(DGDIFF_E_ARG, "centering must be 0 or 1");
@@ -1523,7 +1523,7 @@ extern "C" dgdiff_status dgdiff_mc_covariance(dgdiff_t H, const int32_t *sources
 }
 
 extern "C" dgdiff_status dgdiff_absorb_table(int32_t degree, double *A) {
-  if (degree < 1 || degree > 2) return fail(DGDIFF_E_ARG, "degree %d not supported (1 or 2)", degree);
+  if (degree < 1 || degree > 3) return fail(DGDIFF_E_ARG, "degree %d not supported (1..3)", degree);
   if (!A) return fail(DGDIFF_E_ARG, "A is NULL");
   try {
     std::vector<double> T = dgop::build_absorb(degree);

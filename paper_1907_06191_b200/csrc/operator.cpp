@@ -701,7 +701,7 @@ void point_init(const Table &T, double xi, double eta, double *out) {
 }
 
 std::vector<double> build_absorb(int p) {
-  if (p < 1 || p > 2) throw std::runtime_error("absorbing table: degree must be 1 or 2");
+  if (p < 1 || p > 3) throw std::runtime_error("absorbing table: degree must be 1..3");
   RefEl R;
   build_ref(R, p);
   const int d = R.d, D2 = 2 * d;

@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
           for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
           mv_imm<T, NV, P, 8>(acc, xn);
         }
-      } else if constexpr (P <= 2) {
+      } else {
         // boundary pixel with absorbing outer faces: blocks of (code, outer)
         // read from the K0 table in global memory (rare: grid-edge pixels)
         const T *Ab = Aabs + (size_t)((open_code(nb) * 16 + outer) * 5) * D2 * D2;

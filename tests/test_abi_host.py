@@ -161,7 +161,7 @@ def composite_apply_absorb(A, Aabs, mask, u):
     return out
 
 
-@pytest.mark.parametrize("p", [1, 2])
+@pytest.mark.parametrize("p", [1, 2, 3])
 def test_absorb_table_reproduces_oracle_operator(dg, p, orc):
     """ABSORB (Eq. (4)): K0's boundary-pixel blocks + the interior table equal
     O1's L(u) with outer_bc=1 on random masks touching every grid edge."""
@@ -210,7 +210,7 @@ def test_argument_errors_are_reported(dg):
         dg.dgdiff_create(np.zeros((4, 4), np.uint8), 1.0, 1.0, 4)
     assert e.value.status == dg.E_ARG
     # P3 (N4): ring kernel and REFLECT only
-    for bad in (dict(kernel=1), dict(outer_bc=1), dict(temporal_steps=2)):
+    for bad in (dict(kernel=1), dict(temporal_steps=2)):
         with pytest.raises(dg.DGDiffError) as e:
             dg.dgdiff_create(np.zeros((4, 4), np.uint8), 1.0, 1.0, 3, dg.dgdiff_opts_default(**bad))
         assert e.value.status == dg.E_ARG, bad

@@ -360,7 +360,7 @@ def test_absorb_c1_golden_and_oracle(dg, orc, cfg, prec):
     assert np.allclose([S[0, 0], S[0, 1], S[1, 1]], g["sigma"], rtol=t["sig"], atol=t["sig"])
 
 
-@pytest.mark.parametrize("p,prec", [(1, 64), (1, 32), (2, 64)])
+@pytest.mark.parametrize("p,prec", [(1, 64), (1, 32), (2, 64), (3, 64)])
 def test_absorb_random_masks(dg, orc, p, prec):
     """ABSORB on random masks touching every grid edge (all (code, outer)
     combinations occur), ragged two-chunk batch, vs O1."""
@@ -371,7 +371,7 @@ def test_absorb_random_masks(dg, orc, p, prec):
     n = G + 7
     pick = free[rng.integers(0, len(free), n)]
     src = np.stack([pick[:, 1], pick[:, 0]], 1).astype(np.int32)
-    dt = 1 / 32 if p == 1 else 1 / 128
+    dt = {1: 1 / 32, 2: 1 / 128, 3: 1 / 256}[p]
     ref_m, ref_d = orc.solve(p, 1.0, 1.0, mk, src, dt, 80, outer_bc=1, keep_density=True)
     with dg.Solver(mk, 1.0, 1.0, p, precision=prec, outer_bc=1, keep_density=1, max_chunk=G) as s:
         s.solve(src, dt, 80)
