@@ -222,13 +222,15 @@ __global__ void __launch_bounds__(FusedGeom<T>::THREADS, 1)
       return nring[sl];
     };
     // U1 row r lives in slot r mod 3 (base index a1), U2 row r in slot r mod 4 (a2)
+    // (slot bases come from the row's ring metadata, valid while its u row
+    // or a later one is held: no shared base table, so no barrier to publish it)
     auto u1t = [&](int r, int idx) -> T * {
       const int sl = ((r % 3) + 3) % 3;
-      return u1s + ((size_t)sl * SLOT1 + (idx - rowinfo[sl])) * D2 * G + lane;
+      return u1s + ((size_t)sl * SLOT1 + (idx - meta[seq(r) % Q].a1)) * D2 * G + lane;
     };
     auto u2t = [&](int r, int idx) -> T * {
       const int sl = ((r % 4) + 4) % 4;
-      return u2s + ((size_t)sl * SLOT2 + (idx - rowinfo[3 + sl])) * D2 * G + lane;
+      return u2s + ((size_t)sl * SLOT2 + (idx - meta[seq(r) % Q].a2)) * D2 * G + lane;
     };
     const int i0 = max(0, jb0 - 2), i1 = min(ny - 1, jb1 + 1);   // U1 rows
     const int iend = jb1 + 2;                                      // u'(jb1-1) is done at i = jb1+2
@@ -281,7 +283,6 @@ __global__ void __launch_bounds__(FusedGeom<T>::THREADS, 1)
             m = meta[seq(i) % Q];
             mn = (i + 1 <= hi) ? meta[seq(i + 1) % Q] : m;
             ms = (i - 1 >= lo) ? meta[seq(i - 1) % Q] : m;
-            if (tid == 0) rowinfo[i % 3] = m.a1;
             nitem = m.b1 - m.a1;
           }
           if (i == i0) prefetch(i);
@@ -289,7 +290,6 @@ __global__ void __launch_bounds__(FusedGeom<T>::THREADS, 1)
           // ---- phase B: U2(i-1) over [a2, b2), then u'(i-3) over [c0, c1)
           items(i, n2, c0, n3);
           m2 = meta[seq(max(lo, min(hi, i - 1))) % Q];
-          if (n2 > 0 && tid == 0) rowinfo[3 + (((i - 1) % 4) + 4) % 4] = m2.a2;
           cur_a = pf_a;
           cur_nb = pf_nb;
 #pragma unroll
@@ -297,7 +297,8 @@ __global__ void __launch_bounds__(FusedGeom<T>::THREADS, 1)
           if (i + 1 <= iend) prefetch(i + 1);
           nitem = n2 + n3;
         }
-        named_bar(1, NT);
+        // (no barrier here: the slot a phase writes was last read before the
+        // barrier that ended the previous phase)
         for (int it = w; it < nitem; it += NC) {
           const T *ps, *pe, *pw, *pn, *pq, *zs = nullptr;
           T *out;
