@@ -486,7 +486,7 @@ static size_t tsize(const dgdiff_s *H) { return H->o.precision == 32 ? 4 : 8; }
 // use_fused); its groups are 32 sources (one value per lane)
 static bool use_fused(const dgdiff_s *H) {
   if (H->p != 1 || H->o.kernel == 1 || H->o.kernel == 2 || H->o.kernel == 9) return false;
-  return H->o.temporal_steps == 2;
+  return H->o.temporal_steps == 2 || H->o.temporal_steps == 3;   // 3: K3b, decoupled warp roles
 }
 // values per lane of the state layout: v1/v2 16-byte lanes; ring P1 16-byte,
 // ring P2 8-byte lanes (tile size); fused step one value per lane
@@ -901,19 +901,21 @@ extern "C" dgdiff_status dgdiff_create(dgdiff_t *out, const uint8_t *mask, int32
   if (opts) o = *opts; else dgdiff_opts_default(&o);
   if (o.precision != 32 && o.precision != 64) return fail(DGDIFF_E_ARG, "precision must be 32 or 64");
   if (o.outer_bc != 0 && o.outer_bc != 1) return fail(DGDIFF_E_ARG, "outer_bc must be 0 (REFLECT) or 1 (ABSORB)");
-  if (o.outer_bc == 1 && (o.kernel == 1 || o.kernel == 2 || o.temporal_steps == 2))
+  if (o.outer_bc == 1 && (o.kernel == 1 || o.kernel == 2 || o.temporal_steps >= 2))
     return fail(DGDIFF_E_ARG, "outer_bc ABSORB runs on the default ring kernel only");
   if (o.windows < 0 || o.windows > 2) return fail(DGDIFF_E_ARG, "windows must be 0, 1 or 2");
-  if (degree == 3 && (o.kernel == 1 || o.kernel == 2 || o.temporal_steps == 2))
+  if (degree == 3 && (o.kernel == 1 || o.kernel == 2 || o.temporal_steps >= 2))
     return fail(DGDIFF_E_ARG, "P3 (N4) runs on the default ring kernel only");
-  if (o.windows != 0 && (o.kernel == 1 || o.kernel == 2 || o.temporal_steps == 2))
+  if (o.windows != 0 && (o.kernel == 1 || o.kernel == 2 || o.temporal_steps >= 2))
     return fail(DGDIFF_E_ARG, "windows (N1) run on the default ring kernel only");
   if (o.centering != 0 && o.centering != 1) return fail(DGDIFF_E_ARG, "centering must be 0 or 1");
   if (o.element != 0 && o.element != 1) return fail(DGDIFF_E_ARG, "element must be 0 (triangles) or 1 (quadrilaterals)");
-  if (o.element == 1 && (degree > 2 || o.kernel == 1 || o.kernel == 2 || o.temporal_steps == 2))
+  if (o.element == 1 && (degree > 2 || o.kernel == 1 || o.kernel == 2 || o.temporal_steps >= 2))
     return fail(DGDIFF_E_ARG, "quadrilateral Q_p (N4): degree 1 or 2, default ring kernel only");
   if (o.nranks < 1 || o.rank < 0 || o.rank >= o.nranks) return fail(DGDIFF_E_ARG, "bad rank/nranks");
-  if (o.temporal_steps < 0) return fail(DGDIFF_E_ARG, "temporal_steps < 0");
+  if (o.temporal_steps < 0 || o.temporal_steps > 3) return fail(DGDIFF_E_ARG, "temporal_steps must be 0..3");
+  if (o.temporal_steps == 3 && o.precision != 64)
+    return fail(DGDIFF_E_ARG, "temporal_steps 3 (K3b) is fp64 only");
   if (o.max_chunk < 0) return fail(DGDIFF_E_ARG, "max_chunk < 0");
   if (o.mixture_radius < 0 || o.mixture_radius > 2048) return fail(DGDIFF_E_ARG, "mixture_radius must be in [0, 2048]");
   dgdiff_s *H = new dgdiff_s();
@@ -1076,7 +1078,7 @@ static dgdiff_status run_chunk(dgdiff_s *H, int64_t nvalid, int64_t chunk, doubl
       sa.Uin = cur;
       sa.U0 = cur;
       sa.Uout = nxt;
-      cudaError_t e = dgl::launch_step_fused(prec, sa);
+      cudaError_t e = H->o.temporal_steps == 3 ? dgl::launch_dec_f64(sa) : dgl::launch_step_fused(prec, sa);
       if (e != cudaSuccess) return fail(DGDIFF_E_CUDA, "fused step launch: %s", cudaGetErrorString(e));
       std::swap(cur, nxt);
     }

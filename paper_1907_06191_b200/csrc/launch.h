@@ -40,6 +40,8 @@ cudaError_t launch_step_fused(int prec, const StageArgs &a);
 int fused_width(int prec);
 cudaError_t launch_fused_f64(const StageArgs &a);
 cudaError_t launch_fused_f32(const StageArgs &a);
+// K3b: the fused step with decoupled warp roles (fp64 P1, temporal_steps = 3)
+cudaError_t launch_dec_f64(const StageArgs &a);
 
 // per-TU entry points
 cudaError_t launch_v12_f64(int which, int P, bool alpha, const StageArgs &a);

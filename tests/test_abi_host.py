@@ -220,6 +220,11 @@ def test_argument_errors_are_reported(dg):
     with pytest.raises(dg.DGDiffError) as e:
         dg.dgdiff_create(np.zeros((4, 4), np.uint8), 1.0, 1.0, 1, dg.dgdiff_opts_default(outer_bc=2))
     assert e.value.status == dg.E_ARG
+    # K3b is fp64 only; temporal_steps in 0..3
+    for bad in (dict(temporal_steps=3, precision=32), dict(temporal_steps=4)):
+        with pytest.raises(dg.DGDiffError) as e:
+            dg.dgdiff_create(np.zeros((4, 4), np.uint8), 1.0, 1.0, 1, dg.dgdiff_opts_default(**bad))
+        assert e.value.status == dg.E_ARG, bad
     # N1 windows: 0/1 only, and only on the ring kernel
     for bad in (dict(windows=3), dict(windows=1, kernel=1), dict(windows=2, temporal_steps=2)):
         with pytest.raises(dg.DGDiffError) as e:
