@@ -58,10 +58,13 @@ typedef struct {
                              E_ARG), for every element type */
   int32_t centering;      /* 0 = shift each density by its source point (default,
                              reading R12); 1 = by its own mean */
-  int32_t temporal_steps; /* 0 = library choice; 1 = one launch per RK stage
-                             (K2); 2 = fused step (K3: one whole SSP-RK3 step
-                             per launch, temporal blocking over the 3 stages,
-                             degree 1 only -- other degrees use K2) */
+  int32_t temporal_steps; /* 0 = library choice (K2); 1 = one launch per RK
+                             stage (K2); 2 = fused step (K3: one whole SSP-RK3
+                             step per launch, temporal blocking over the 3
+                             stages, lock-step rows; P1 triangles); 3 = fused
+                             step with decoupled warp roles (K3b, fp64 P1,
+                             bit-identical to K2).  Other degrees / elements
+                             use K2; 2 and 3 exclude ABSORB, windows, quads */
   int32_t device;         /* CUDA device ordinal; -1 = current device */
   int32_t rank, nranks;   /* source sharding: rank takes the contiguous block
                              [rank*n/nranks, (rank+1)*n/nranks) of every batch */
