@@ -437,18 +437,18 @@ def test_mixture_free_space_is_gaussian(orc):
     n = 72
     mask = np.zeros((n, n), np.uint8)
     src = [(36, 36), (34, 37), (38, 35)]
-    mom, dens = orc.solve(2, 1.0, 1.0, mask, src, 1 / 128, 1024, keep_density=True)   # Delta = 8, sigma = 4
-    R = 24
+    mom, dens = orc.solve(2, 1.0, 1.0, mask, src, 1 / 128, 512, keep_density=True)   # Delta = 4, sigma = 2.8
+    R = 20
     g = orc.mixture(2, dens, src, mom, R)
     g1 = orc.mixture(2, dens[:1], src[:1], mom[:1], R)
     assert np.abs(g - g1).max() <= 1e-5 * g1.max()
     assert abs(g.sum() - 1.0) < 2e-3
     x = np.arange(-R, R + 1)
-    assert abs((g.sum(axis=0) * x ** 2).sum() - 16.0) < 0.1     # midpoint rule, truncated at 6 sigma
+    assert abs((g.sum(axis=0) * x ** 2).sum() - 8.0) < 0.02 * 8.0   # midpoint rule on node values, O(h^2/sigma^2)
     S, mu = orc.sigma(mom)
     res = orc.residual(g, 1.0, S, mu)
     X, Y = np.meshgrid(x, x)
-    gauss = np.exp(-(X ** 2 + Y ** 2) / 32.0) / (2 * np.pi * 16.0)
+    gauss = np.exp(-(X ** 2 + Y ** 2) / 16.0) / (2 * np.pi * 8.0)
     assert res < 1e-3 * (gauss ** 2).sum()
     # Eq. (9) itself: the fitted Gaussian sampled at the nodes has zero residual
     Si = np.linalg.inv(S)
