@@ -426,6 +426,10 @@ struct dgdiff_s {
   const double *cur_px = nullptr;  // rows of the chunk being solved (points mode)
   double *d_partial = nullptr;
   size_t partial_cap = 0;
+  unsigned *d_wcnt = nullptr;                      // K3c: per-item completion counters
+  size_t wcnt_cap = 0;
+  int2 *d_wtab = nullptr;                          // K3c: (stage, band) order of a group's items
+  int wtab_nb = 0;
   int32_t *d_src = nullptr;
   int64_t src_cap = 0;
   double *d_mom = nullptr;
@@ -573,6 +577,8 @@ static void release(dgdiff_s *H) {
   cudaFree(H->d_src_xy);
   cudaFree(H->d_px);
   cudaFree(H->d_partial);
+  cudaFree(H->d_wcnt);
+  cudaFree(H->d_wtab);
   cudaFree(H->d_src);
   cudaFree(H->d_mom);
   cudaFree(H->d_out);
@@ -913,9 +919,11 @@ extern "C" dgdiff_status dgdiff_create(dgdiff_t *out, const uint8_t *mask, int32
   if (o.element == 1 && (degree > 2 || o.kernel == 1 || o.kernel == 2 || o.temporal_steps >= 2))
     return fail(DGDIFF_E_ARG, "quadrilateral Q_p (N4): degree 1 or 2, default ring kernel only");
   if (o.nranks < 1 || o.rank < 0 || o.rank >= o.nranks) return fail(DGDIFF_E_ARG, "bad rank/nranks");
-  if (o.temporal_steps < 0 || o.temporal_steps > 3) return fail(DGDIFF_E_ARG, "temporal_steps must be 0..3");
+  if (o.temporal_steps < 0 || o.temporal_steps > 4) return fail(DGDIFF_E_ARG, "temporal_steps must be 0..4");
   if (o.temporal_steps == 3 && o.precision != 64)
     return fail(DGDIFF_E_ARG, "temporal_steps 3 (K3b) is fp64 only");
+  if (o.temporal_steps == 4 && o.kernel != 0)
+    return fail(DGDIFF_E_ARG, "temporal_steps 4 (K3c wavefront) runs the ring kernel's items only");
   if (o.max_chunk < 0) return fail(DGDIFF_E_ARG, "max_chunk < 0");
   if (o.mixture_radius < 0 || o.mixture_radius > 2048) return fail(DGDIFF_E_ARG, "mixture_radius must be in [0, 2048]");
   dgdiff_s *H = new dgdiff_s();
@@ -1091,6 +1099,53 @@ static dgdiff_status run_chunk(dgdiff_s *H, int64_t nvalid, int64_t chunk, doubl
     H->st.launches += nsteps;
     H->st.stage_launches += nsteps;
     H->st.stage_bytes += 2.0 * pass * nsteps;
+    H->st.stage_flops += fused_flops_per_step(H, chunk) * nsteps;
+    goto after_stepping;
+  }
+  if (H->o.temporal_steps == 4 && !H->windows) {
+    // K3c: one launch per SSP-RK3 step, stage items in wavefront order
+    const int br = dgl::wave_band_rows();
+    const int nb = (H->ny + br - 1) / br;
+    const size_t ncnt = (size_t)ngroups * 3 * nb * H->nstrips;   // >= the strip-block count
+    if (ncnt > H->wcnt_cap) {
+      cudaFree(H->d_wcnt);
+      H->d_wcnt = nullptr;
+      CK(cudaMalloc(&H->d_wcnt, ncnt * sizeof(unsigned)));
+      H->wcnt_cap = ncnt;
+    }
+    if (H->wtab_nb != nb) {
+      std::vector<int2> wt;
+      // stage k of band b in wavefront b + 2k: an item's inputs (stage k-1,
+      // bands b-1..b+1) all belong to earlier wavefronts
+      for (int w = 0; w < nb + 4; w++)
+        for (int k = 0; k < 3; k++)
+          if (w - 2 * k >= 0 && w - 2 * k < nb) wt.push_back(make_int2(k, w - 2 * k));
+      cudaFree(H->d_wtab);
+      H->d_wtab = nullptr;
+      CK(cudaMalloc(&H->d_wtab, wt.size() * sizeof(int2)));
+      CK(cudaMemcpy(H->d_wtab, wt.data(), wt.size() * sizeof(int2), cudaMemcpyHostToDevice));
+      H->wtab_nb = nb;
+    }
+    CK(cudaMemsetAsync(H->d_wcnt, 0, ncnt * sizeof(unsigned), st));
+    sa.Uin = u;
+    sa.U0 = Ua;
+    sa.Uout = Ub;
+    sa.cs = c;
+    sa.band_rows = br;
+    sa.wave_cnt = H->d_wcnt;
+    sa.wave_tab = H->d_wtab;
+    for (int64_t s = 0; s < nsteps; s++) {
+      sa.wave_epoch = (unsigned)(s + 1);
+      cudaError_t e = dgl::launch_wave(prec, P, sa);
+      if (e != cudaSuccess) return fail(DGDIFF_E_CUDA, "wavefront step launch: %s", cudaGetErrorString(e));
+    }
+    if (e1) {
+      CK(cudaEventRecord(e1, st));
+      H->ev_launches_pending += nsteps;
+    }
+    H->st.launches += nsteps;
+    H->st.stage_launches += nsteps;
+    H->st.stage_bytes += 4.0 * pass * nsteps;   // u read + u written + U1, U2 written back
     H->st.stage_flops += fused_flops_per_step(H, chunk) * nsteps;
     goto after_stepping;
   }

@@ -27,6 +27,11 @@ struct StageArgs {
   const int4 *gbox = nullptr;
   int wr = 0;
   int band_rows = 0;                // ring: max rows per band (0 = heuristic)
+  // K3c wavefront step: per-item completion counters, (stage, band) order of a
+  // group's items, 1-based step index within the chunk
+  unsigned *wave_cnt = nullptr;
+  const int2 *wave_tab = nullptr;
+  unsigned wave_epoch = 0;
   cudaStream_t st = nullptr;
 };
 
@@ -42,6 +47,11 @@ cudaError_t launch_fused_f64(const StageArgs &a);
 cudaError_t launch_fused_f32(const StageArgs &a);
 // K3b: the fused step with decoupled warp roles (fp64 P1, temporal_steps = 3)
 cudaError_t launch_dec_f64(const StageArgs &a);
+
+// K3c: one SSP-RK3 step as an L2-resident wavefront of ring items (temporal_steps
+// = 4; P1/P2 triangles, REFLECT): a.Uin = u (in place), a.U0 = U1, a.Uout = U2
+cudaError_t launch_wave(int prec, int P, const StageArgs &a);
+int wave_band_rows();
 
 // per-TU entry points
 cudaError_t launch_v12_f64(int which, int P, bool alpha, const StageArgs &a);

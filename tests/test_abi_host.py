@@ -220,8 +220,9 @@ def test_argument_errors_are_reported(dg):
     with pytest.raises(dg.DGDiffError) as e:
         dg.dgdiff_create(np.zeros((4, 4), np.uint8), 1.0, 1.0, 1, dg.dgdiff_opts_default(outer_bc=2))
     assert e.value.status == dg.E_ARG
-    # K3b is fp64 only; temporal_steps in 0..3
-    for bad in (dict(temporal_steps=3, precision=32), dict(temporal_steps=4)):
+    # K3b is fp64 only; K3c (4) needs the ring kernel; temporal_steps in 0..4
+    for bad in (dict(temporal_steps=3, precision=32), dict(temporal_steps=4, kernel=1), dict(temporal_steps=5),
+                dict(temporal_steps=4, outer_bc=1), dict(temporal_steps=4, windows=1)):
         with pytest.raises(dg.DGDiffError) as e:
             dg.dgdiff_create(np.zeros((4, 4), np.uint8), 1.0, 1.0, 1, dg.dgdiff_opts_default(**bad))
         assert e.value.status == dg.E_ARG, bad

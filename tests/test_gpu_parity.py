@@ -855,3 +855,22 @@ def test_k3b_decoupled_step_bitwise_equals_per_stage(dg, orc, cfg, nsteps):
         with dg.Solver(cfg.mask("c1"), 1.0, 1.0, 1, temporal_steps=3, keep_density=1) as s:
             s.solve(cfg.sources("c1"), c.dt, c.nsteps)
             assert rel_l2(s.density(0), ref_d[0]) <= 1e-12
+
+
+@pytest.mark.parametrize("degree,prec", [(1, 64), (1, 32), (2, 64), (2, 32)])
+def test_k3c_wavefront_step_bitwise_equals_per_stage(dg, cfg, degree, prec):
+    """K3c (temporal_steps = 4: one launch per SSP-RK3 step, the ring kernel's
+    items of all three stages in wavefront order with per-item completion
+    counters) does each pixel's arithmetic exactly as K2: moments and
+    densities bit-identical on the c3 substrate (32 strips, several bands,
+    two source groups in a chunk and a ragged second chunk), several steps."""
+    m = cfg.mask("c3")
+    src = cfg.sources("c3", 200)[:150]
+    dt = 1 / 32 if degree == 1 else 1 / 128
+    out = {}
+    for ts in (0, 4):
+        with dg.Solver(m, 1.0, 1.0, degree, precision=prec, temporal_steps=ts, keep_density=1, max_chunk=128) as s:
+            s.solve(src, dt, 5)
+            out[ts] = (s.moments(), s.density(149), s.density(3))
+    for a, b in zip(out[4], out[0]):
+        assert np.array_equal(a, b)
