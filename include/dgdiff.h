@@ -63,8 +63,13 @@ typedef struct {
                              step per launch, temporal blocking over the 3
                              stages, lock-step rows; P1 triangles); 3 = fused
                              step with decoupled warp roles (K3b, fp64 P1,
-                             bit-identical to K2).  Other degrees / elements
-                             use K2; 2 and 3 exclude ABSORB, windows, quads */
+                             bit-identical to K2); 4 = wavefront step (K3c:
+                             one launch per step, the K2 items of all three
+                             stages ordered as a skewed wavefront with
+                             per-item completion counters; P1/P2 triangles,
+                             fp64/fp32, bit-identical to K2).  Other degrees /
+                             elements use K2; 2..4 exclude ABSORB, windows,
+                             quads, P3; 4 needs kernel 0 */
   int32_t device;         /* CUDA device ordinal; -1 = current device */
   int32_t rank, nranks;   /* source sharding: rank takes the contiguous block
                              [rank*n/nranks, (rank+1)*n/nranks) of every batch */

@@ -10,7 +10,8 @@
 // Every dependency has a smaller number, and a CTA takes its items in
 // increasing order, so the smallest unfinished item can always run.
 //
-// Stage k of band b runs about k bands behind stage 0, so the U1 / U2 rows a
+// Stage k of band b sits in wavefront b + 2k, so an item's inputs were all
+// written in earlier wavefronts.  Stage k runs 2k bands behind stage 0: the U1 / U2 rows a
 // stage reads were written a few hundred items earlier and are still in L2,
 // and so are the u rows of the alpha terms: HBM sees u read once, u written
 // once, U1 and U2 written once (their dirty lines are evicted) -- 4 state
@@ -36,6 +37,10 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ void red_release_add(unsigned *p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+constexpr int WAVE_WQ = 8;   // item completion slots per CTA
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
@@ -59,13 +64,14 @@ __device__ __forceinline__ void wave_item(int item, int nstrips, int ngroups, in
 }
 
 template <typename T, int NV, int P>
-__global__ void __launch_bounds__(RingGeom<T, NV, P, true>::THREADS, 1)
+__global__ void __launch_bounds__(RingGeom<T, NV, P, true>::THREADS + 32, 1)
     k_step_wave(T *u, T *U1, T *U2, const int4 *__restrict__ nbr, const int4 *__restrict__ rowtab, int nact, int ny,
                 int nstrips, int sblk, int ngroups, int gblk, int band_rows, int nbands, const int2 *__restrict__ wtab, int nitems,
                 T c1, T c2, T c3, T a2, T a3, unsigned *cnt, unsigned epoch, int max_ahead, int n1_use,
                 int n2_use) {
   using Gm = RingGeom<T, NV, P, true>;
   static_assert(!is_quad<P>() && P <= 2, "wavefront step: P1 / P2 triangles");
+  static_assert(Gm::SMEM + 2 * WAVE_WQ * 8 <= Gm::SMEM_MAX, "no room for the completion slots");
   constexpr int G = Gm::G, D2 = Gm::D2, PXB = Gm::PXB, Q = RING_Q, NC = Gm::NC;
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char *ring1 = smem;
@@ -75,20 +81,44 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, true>::THREADS, 1)
   RowMeta *meta = reinterpret_cast<RowMeta *>(smem + Gm::OFF_META);
   int4 *rt = reinterpret_cast<int4 *>(smem + Gm::OFF_RT);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  // item completion inside the CTA: consumers arrive on done[i % WQ] (count
+  // NC) after their stores; the publisher warp turns that into one gpu-scope
+  // release per item and frees the slot through pubd[i % WQ]
+  __shared__ uint64_t done[WAVE_WQ], pubd[WAVE_WQ];
   if (tid == 0) {
     for (int q = 0; q < Q; q++) {
       mbar_init(&full[q], 1);
       mbar_init(&empty[q], NC);
     }
+    for (int q = 0; q < WAVE_WQ; q++) {
+      mbar_init(&done[q], NC);
+      mbar_init(&pubd[q], 1);
+    }
     fence_mbar_init();
   }
   __syncthreads();
   const size_t gstride = (size_t)nact * D2 * G;
-  const unsigned target = epoch * (unsigned)NC;   // NC counts per item per step
+  const unsigned target = epoch;                  // one count per item per step
   const int nsb = (nstrips + sblk - 1) / sblk;      // strip blocks
   // completion counter of item (k, g, b, s)
   auto cidx = [&](int k, int g, int b, int s) { return (((size_t)g * 3 + k) * nbands + b) * nsb + s; };
 
+  if (w == NC + 1) {
+    // =========================== publisher warp ===========================
+    uint32_t it = 0;
+    for (int item = blockIdx.x; item < nitems; item += gridDim.x, it++) {
+      int k, g, b, sb;
+      wave_item(item, nsb, ngroups, gblk, 3 * nbands, wtab, k, g, b, sb);
+      mbar_wait(&done[it % WAVE_WQ], (it / WAVE_WQ) & 1);
+      if (lane == 0) {
+        __threadfence();
+        red_release_add(cnt + cidx(k, g, b, sb), 1u);
+        mbar_arrive(&pubd[it % WAVE_WQ]);
+      }
+      __syncwarp();
+    }
+    return;
+  }
   if (w == NC) {
     // =========================== producer warp ===========================
     uint32_t *rv = reinterpret_cast<uint32_t *>(rt + RING_MAXBAND + 4);
@@ -98,6 +128,9 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, true>::THREADS, 1)
       wave_item(item, nsb, ngroups, gblk, 3 * nbands, wtab, k, g, b, sb);
       const int jb0 = b * band_rows, jb1 = min(ny, jb0 + band_rows);
       const int lo = max(0, jb0 - 1), hi = min(ny - 1, jb1);
+      // first strip's row table, loaded before the dependency wait (read-only)
+      int4 pre = make_int4(0, 0, 0, 0);
+      if (hi - lo < 32 && lo + lane <= hi) pre = __ldg(&rowtab[(size_t)(sb * sblk) * ny + lo + lane]);
       if (k > 0) {
         // wait for the 3 x 3 items of stage k-1 that write this item's input
         // (bands b-1..b+1, strip blocks sb-1..sb+1)
@@ -113,7 +146,11 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, true>::THREADS, 1)
       const T *Ug = (k == 0 ? u : k == 1 ? U1 : U2) + g * gstride;
       for (int s = sb * sblk; s < min(nstrips, sb * sblk + sblk); s++) {
       __syncwarp();
-      for (int r = lo + lane; r <= hi; r += 32) rt[r - lo] = __ldg(&rowtab[(size_t)s * ny + r]);
+      if (s == sb * sblk && hi - lo < 32) {
+        if (lo + lane <= hi) rt[lane] = pre;
+      } else {
+        for (int r = lo + lane; r <= hi; r += 32) rt[r - lo] = __ldg(&rowtab[(size_t)s * ny + r]);
+      }
       __syncwarp();
       for (int r0 = lo; r0 <= hi;) {
         const int r = r0 + lane;
@@ -179,8 +216,8 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, true>::THREADS, 1)
   }
 
   // ============================= consumer warps ============================
-  uint32_t Lbase = 0;
-  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+  uint32_t Lbase = 0, it = 0;
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x, it++) {
     int k, g, b, sb;
     wave_item(item, nsb, ngroups, gblk, 3 * nbands, wtab, k, g, b, sb);
     const int jb0 = b * band_rows, jb1 = min(ny, jb0 + band_rows);
@@ -284,21 +321,26 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, true>::THREADS, 1)
       for (int r = rel_next; r <= hi; r++) mbar_arrive(&empty[seq(r) % Q]);
     Lbase += (uint32_t)(hi - lo + 1);
     }   // strips of the block
-    // publish: this warp's stores, then one count per warp (NC per item)
+    // hand the item to the publisher (slot reuse waits for its release)
     fence_proxy_async_global();
-    __threadfence();
     __syncwarp();
-    if (lane == 0) atomicAdd(cnt + cidx(k, g, b, sb), 1u);
+    if (lane == 0) {
+      if (it >= WAVE_WQ) mbar_wait(&pubd[it % WAVE_WQ], ((it / WAVE_WQ) - 1) & 1);
+      mbar_arrive(&done[it % WAVE_WQ]);
+    }
   }
 }
 
-// rows per band of the wavefront (small: the live rows of u, U1 and U2 of one
-// group must stay in L2); DGDIFF_WAVE_BAND overrides
+// rows per band of the wavefront; DGDIFF_WAVE_BAND overrides.  Bands of 2-4
+// rows keep the live rows of u, U1, U2 in L2 (c4: DRAM 107 GB per step vs
+// K2's 165 GB) but the per-item pipeline then runs at ~1.3 us per row and
+// ~1 us per item (43 / 33 ms per c4 step); 32-row bands amortise the item
+// cost and lose most L2 hits (28.3 ms, K2 28.0 ms) -- DESIGN.md section 6
 inline int wave_band_rows() {
   static const int v = [] {
     const char *e = getenv("DGDIFF_WAVE_BAND");
     const int x = e ? atoi(e) : 0;
-    return x > 0 ? std::min(x, RING_MAXBAND) : 4;
+    return x > 0 ? std::min(x, RING_MAXBAND - 2) : 32;
   }();
   return v;
 }
@@ -309,6 +351,21 @@ inline int wave_sblk() {
     const int x = e ? atoi(e) : 0;
     return x > 0 ? x : 4;
   }();
+  return v;
+}
+// ring-1 pixel slots in use (DGDIFF_WAVE_N1; 0 = the whole ring): the
+// wavefront reads from L2, so it wants as many rows in flight as fit
+inline int wave_n1() {
+  static const int v = [] {
+    const char *e = getenv("DGDIFF_WAVE_N1");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+// diagnostic (DGDIFF_WAVE_NODEP=1): skip the dependency waits -- WRONG results,
+// timing only (how much the wavefront's dependency chain costs)
+inline bool wave_nodep() {
+  static const bool v = getenv("DGDIFF_WAVE_NODEP") && atoi(getenv("DGDIFF_WAVE_NODEP")) == 1;
   return v;
 }
 // source groups per wavefront block (DGDIFF_WAVE_GBLK; 0 = all groups)
@@ -340,12 +397,12 @@ cudaError_t launch_wave(const dgl::StageArgs &a) {
   const int nitems = 3 * nbands * ((a.nstrips + sblk - 1) / sblk) * a.ngroups;
   const int grid = std::min(nitems, a.nsm);
   const double c = a.cs;
-  k_step_wave<T, NV, P><<<grid, Gm::THREADS, Gm::SMEM, a.st>>>(
+  k_step_wave<T, NV, P><<<grid, Gm::THREADS + 32, Gm::SMEM, a.st>>>(
       (T *)a.Uin, (T *)a.U0, (T *)a.Uout, a.nbr, a.rowtab, a.nact, a.ny, a.nstrips, sblk, a.ngroups, wave_gblk(a.ngroups),
       band_rows, nbands,
       a.wave_tab, nitems, (T)c, (T)(0.25 * c), (T)((2.0 / 3.0) * c), (T)0.75, (T)(1.0 / 3.0), a.wave_cnt,
-      a.wave_epoch, std::max(Gm::ROWS_MIN, std::min(RING_Q - 1, alpha_max_ahead(a, true))),
-      std::max(Gm::ROWS_MIN * (Gm::W + 2 * Gm::HALO), std::min(Gm::N1, a.n1_use_na > 0 ? a.n1_use_na : Gm::N1)),
+      wave_nodep() ? 0u : a.wave_epoch, std::max(Gm::ROWS_MIN, std::min(RING_Q - 1, alpha_max_ahead(a, true))),
+      std::max(Gm::ROWS_MIN * (Gm::W + 2 * Gm::HALO), std::min(Gm::N1, wave_n1() > 0 ? wave_n1() : Gm::N1)),
       std::max(Gm::ROWS_MIN * Gm::W, std::min(Gm::N2, a.n2_use > 0 ? a.n2_use : Gm::N2)));
   return cudaGetLastError();
 }
