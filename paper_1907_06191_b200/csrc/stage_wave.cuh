@@ -41,6 +41,9 @@ __device__ __forceinline__ void red_release_add(unsigned *p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 constexpr int WAVE_WQ = 8;   // item completion slots per CTA
+#ifndef DGDIFF_WAVE_NC
+#define DGDIFF_WAVE_NC 8     // consumer warps (the ring kernel's NC for P1 fp64)
+#endif
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
@@ -64,7 +67,7 @@ __device__ __forceinline__ void wave_item(int item, int nstrips, int ngroups, in
 }
 
 template <typename T, int NV, int P>
-__global__ void __launch_bounds__(RingGeom<T, NV, P, true>::THREADS + 32, 1)
+__global__ void __launch_bounds__((DGDIFF_WAVE_NC + 2) * 32, 1)
     k_step_wave(T *u, T *U1, T *U2, const int4 *__restrict__ nbr, const int4 *__restrict__ rowtab, int nact, int ny,
                 int nstrips, int sblk, int ngroups, int gblk, int band_rows, int nbands, const int2 *__restrict__ wtab, int nitems,
                 T c1, T c2, T c3, T a2, T a3, unsigned *cnt, unsigned epoch, int max_ahead, int n1_use,
@@ -72,7 +75,7 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, true>::THREADS + 32, 1)
   using Gm = RingGeom<T, NV, P, true>;
   static_assert(!is_quad<P>() && P <= 2, "wavefront step: P1 / P2 triangles");
   static_assert(Gm::SMEM + 2 * WAVE_WQ * 8 <= Gm::SMEM_MAX, "no room for the completion slots");
-  constexpr int G = Gm::G, D2 = Gm::D2, PXB = Gm::PXB, Q = RING_Q, NC = Gm::NC;
+  constexpr int G = Gm::G, D2 = Gm::D2, PXB = Gm::PXB, Q = RING_Q, NC = DGDIFF_WAVE_NC;
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char *ring1 = smem;
   int4 *nbr_ring = reinterpret_cast<int4 *>(smem + Gm::OFF_NB);
@@ -397,7 +400,7 @@ cudaError_t launch_wave(const dgl::StageArgs &a) {
   const int nitems = 3 * nbands * ((a.nstrips + sblk - 1) / sblk) * a.ngroups;
   const int grid = std::min(nitems, a.nsm);
   const double c = a.cs;
-  k_step_wave<T, NV, P><<<grid, Gm::THREADS + 32, Gm::SMEM, a.st>>>(
+  k_step_wave<T, NV, P><<<grid, (DGDIFF_WAVE_NC + 2) * 32, Gm::SMEM, a.st>>>(
       (T *)a.Uin, (T *)a.U0, (T *)a.Uout, a.nbr, a.rowtab, a.nact, a.ny, a.nstrips, sblk, a.ngroups, wave_gblk(a.ngroups),
       band_rows, nbands,
       a.wave_tab, nitems, (T)c, (T)(0.25 * c), (T)((2.0 / 3.0) * c), (T)0.75, (T)(1.0 / 3.0), a.wave_cnt,
