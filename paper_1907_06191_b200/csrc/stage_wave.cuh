@@ -71,7 +71,7 @@ __global__ void __launch_bounds__((DGDIFF_WAVE_NC + 2) * 32, 1)
     k_step_wave(T *u, T *U1, T *U2, const int4 *__restrict__ nbr, const int4 *__restrict__ rowtab, int nact, int ny,
                 int nstrips, int sblk, int ngroups, int gblk, int band_rows, int nbands, const int2 *__restrict__ wtab, int nitems,
                 T c1, T c2, T c3, T a2, T a3, unsigned *cnt, unsigned epoch, int max_ahead, int n1_use,
-                int n2_use) {
+                int n2_use, int diag) {
   using Gm = RingGeom<T, NV, P, true>;
   static_assert(!is_quad<P>() && P <= 2, "wavefront step: P1 / P2 triangles");
   static_assert(Gm::SMEM + 2 * WAVE_WQ * 8 <= Gm::SMEM_MAX, "no room for the completion slots");
@@ -131,7 +131,8 @@ __global__ void __launch_bounds__((DGDIFF_WAVE_NC + 2) * 32, 1)
       wave_item(item, nsb, ngroups, gblk, 3 * nbands, wtab, k, g, b, sb);
       const int jb0 = b * band_rows, jb1 = min(ny, jb0 + band_rows);
       const int lo = max(0, jb0 - 1), hi = min(ny - 1, jb1);
-      // first strip's row table, loaded before the dependency wait (read-only)
+      // first strip's row table, loaded before the dependency wait (read-only;
+      // prefetching it one item ahead measured no better)
       int4 pre = make_int4(0, 0, 0, 0);
       if (hi - lo < 32 && lo + lane <= hi) pre = __ldg(&rowtab[(size_t)(sb * sblk) * ny + lo + lane]);
       if (k > 0) {
@@ -259,6 +260,7 @@ __global__ void __launch_bounds__((DGDIFF_WAVE_NC + 2) * 32, 1)
         mc = meta[seq(j) % Q];
       }
       if (j >= jb1) break;
+      if (diag) continue;   // diagnostic: stream through the ring without computing
       const int a = mc.c0 + (f - cum);
       int sl2 = mc.p2 + (a - mc.c0);
       if (sl2 >= Gm::N2) sl2 -= Gm::N2;
@@ -406,7 +408,8 @@ cudaError_t launch_wave(const dgl::StageArgs &a) {
       a.wave_tab, nitems, (T)c, (T)(0.25 * c), (T)((2.0 / 3.0) * c), (T)0.75, (T)(1.0 / 3.0), a.wave_cnt,
       wave_nodep() ? 0u : a.wave_epoch, std::max(Gm::ROWS_MIN, std::min(RING_Q - 1, alpha_max_ahead(a, true))),
       std::max(Gm::ROWS_MIN * (Gm::W + 2 * Gm::HALO), std::min(Gm::N1, wave_n1() > 0 ? wave_n1() : Gm::N1)),
-      std::max(Gm::ROWS_MIN * Gm::W, std::min(Gm::N2, a.n2_use > 0 ? a.n2_use : Gm::N2)));
+      std::max(Gm::ROWS_MIN * Gm::W, std::min(Gm::N2, a.n2_use > 0 ? a.n2_use : Gm::N2)),
+      getenv("DGDIFF_WAVE_DIAG") ? 1 : 0);
   return cudaGetLastError();
 }
 
