@@ -73,8 +73,16 @@ typedef struct {
   int32_t device;         /* CUDA device ordinal; -1 = current device */
   int32_t rank, nranks;   /* source sharding: rank takes the contiguous block
                              [rank*n/nranks, (rank+1)*n/nranks) of every batch */
-  const void *nccl_id;    /* ncclUniqueId* (128 bytes), required if nranks > 1;
-                             with nranks == 1 it creates a one-rank communicator */
+  const void *nccl_id;    /* ncclUniqueId* (128 bytes): the handle joins an
+                             NCCL communicator of nranks ranks (with nranks == 1
+                             a one-rank communicator).  NULL with nranks > 1 =
+                             LOGICAL rank: no communicator; the handle solves
+                             its shard only and its [n][6] moment table holds
+                             zeros in the other ranks' rows; dgdiff_covariance
+                             then fails with E_STATE and the caller sums the
+                             ranks' tables (dgdiff_source_moments) and calls
+                             dgdiff_covariance_table (the same sum NCCL would
+                             do: exact, so Sigma is bitwise that of nranks = 1) */
   int32_t keep_density;   /* 1: keep the final states of the last source chunk for
                              dgdiff_get_density (tests); 0 (default) */
   int32_t max_chunk;      /* max sources resident per chunk; 0 = fit device memory */
@@ -172,6 +180,12 @@ dgdiff_status dgdiff_solve_batch_points(dgdiff_t, const double *points, int64_t 
  * symmetric), mu[2] (nullable) the mixture mean.  Synchronises. */
 dgdiff_status dgdiff_covariance(dgdiff_t, double delta, double sigma[4], double mu[2]);
 
+/* K5 alone: Sigma and mu (as dgdiff_covariance, the handle's centering) of a
+ * caller-provided moment table mom [n][6] (host, copied), e.g. the sum of
+ * the zero-padded tables of the logical ranks of one batch.  Errors:
+ * E_ARG (NULL, n < 1), E_DEGENERATE, E_NONFINITE.  Synchronises. */
+dgdiff_status dgdiff_covariance_table(dgdiff_t, const double *mom, int64_t n, double sigma[4], double mu[2]);
+
 /* The mixture model u = (1/m) sum_i u_i of the centred, normalised densities
  * sampled at the displacement nodes (dx, dy) in [-R, R]^2 (pixel
  * units, R = opts.mixture_radius): u_i(dx, dy) = value of the DG solution of
@@ -268,6 +282,9 @@ typedef struct {
   int64_t n_active;        /* extracellular pixels */
   int64_t chunk;           /* sources per chunk of the last solve */
   int64_t h2d_bytes, d2h_bytes; /* host<->device bytes moved by the last solve+covariance */
+  int64_t env_overrides;   /* tuning knobs taken from the environment (always 0
+                              in product builds: they ignore the environment) */
+  int64_t tuning_build;    /* 1 if the library was built with -DDGDIFF_TUNING */
 } dgdiff_stats_t;
 
 /* Enable (1) / disable (0) CUDA-event timing of the stage launches. */

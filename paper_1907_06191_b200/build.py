@@ -17,6 +17,11 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdgdiff.so")
+# tuning build (experiments only): -DDGDIFF_TUNING makes the library read its
+# DGDIFF_* tuning knobs from the environment; it goes to a separate library
+# (loaded by dgdiff.py only when DGDIFF_TUNING_LIB=1) so the product library
+# never does
+LIB_TUNING = os.path.join(HERE, "libdgdiff_tuning.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -27,6 +32,7 @@ SOURCES = ["dgdiff.cu", "launch.cu", "stage_v12_f64.cu", "stage_v12_f32.cu", "st
 HEADERS = ["kernels.cuh", "operator.h", "stage_imm.cuh", "stage_ring.cuh", "stage_v12.cuh", "launch.h",
            "step_fused.cuh", "step_dec.cuh", "stage_wave.cuh", "mc_walk.cuh"]
 OBJDIR = os.path.join(HERE, "build_obj")
+OBJDIR_TUNING = os.path.join(HERE, "build_obj_tuning")
 
 
 def _stale(target, deps):
@@ -55,10 +61,11 @@ def build_tables(force=False) -> str:
     return TABLES
 
 
-def _compile(src, verbose):
+def _compile(src, verbose, tuning=False):
     """nvcc -c one translation unit (skipped when its object is fresh)."""
-    os.makedirs(OBJDIR, exist_ok=True)
-    obj = os.path.join(OBJDIR, os.path.basename(src) + ".o")
+    objdir = OBJDIR_TUNING if tuning else OBJDIR
+    os.makedirs(objdir, exist_ok=True)
+    obj = os.path.join(objdir, os.path.basename(src) + ".o")
     deps = [src, TABLES] + [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "dgdiff.h")]
     if not _stale(obj, deps):
         return obj
@@ -67,6 +74,8 @@ def _compile(src, verbose):
            "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-c", src, "-o", tmp]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
+    if tuning:
+        cmd.insert(1, "-DDGDIFF_TUNING")
     r = subprocess.run(cmd, capture_output=True, text=True)
     if verbose or r.returncode:
         sys.stderr.write(r.stdout + r.stderr)
@@ -76,24 +85,27 @@ def _compile(src, verbose):
     return obj
 
 
-def build_dgdiff(force=False, verbose=False) -> str:
-    """Compile every TU in parallel (nvcc, sm_100a) and link libdgdiff.so."""
+def build_dgdiff(force=False, verbose=False, tuning=False) -> str:
+    """Compile every TU in parallel (nvcc, sm_100a) and link libdgdiff.so
+    (tuning=True: libdgdiff_tuning.so, see LIB_TUNING)."""
+    lib = LIB_TUNING if tuning else LIB
+    objdir = OBJDIR_TUNING if tuning else OBJDIR
     from concurrent.futures import ThreadPoolExecutor
     build_tables(force=force)
     srcs = [os.path.join(CSRC, f) for f in SOURCES]
     if force:
         for f in SOURCES:
-            o = os.path.join(OBJDIR, f + ".o")
+            o = os.path.join(objdir, f + ".o")
             if os.path.exists(o):
                 os.remove(o)
     with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
-        objs = list(ex.map(lambda f: _compile(f, verbose), srcs))
-    if not force and not _stale(LIB, objs + [__file__]):
-        return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
+        objs = list(ex.map(lambda f: _compile(f, verbose, tuning), srcs))
+    if not force and not _stale(lib, objs + [__file__]):
+        return lib
+    tmp = lib + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp] + objs + ["-ldl"])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 def build_all(force=False, verbose=False):
@@ -103,5 +115,8 @@ def build_all(force=False, verbose=False):
 
 
 if __name__ == "__main__":
-    build_all(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    if "--tuning" in sys.argv:
+        print(build_dgdiff(force="--force" in sys.argv, verbose="-v" in sys.argv, tuning=True))
+    else:
+        build_all(force="--force" in sys.argv, verbose="-v" in sys.argv)
+        print(LIB)

@@ -266,11 +266,22 @@ __global__ void __launch_bounds__(256) k_finalize(const double *__restrict__ mom
 }
 
 // canonical fp64 copy of one source's state: out[a][k]
+// (N1 windows: outside group g's maintained range [grange.x, grange.y) the
+// registers are not maintained and the density is exactly zero)
 template <typename T, int NV, int D2>
-__global__ void k_gather(const T *__restrict__ U, int nact, int g, int slot, double *__restrict__ out) {
+__global__ void k_gather(const T *__restrict__ U, int nact, int g, int slot, double *__restrict__ out,
+                         const int2 *__restrict__ grange /* nullable */) {
   constexpr int G = 32 * NV;
   int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r >= (int64_t)nact * D2) return;
+  if (grange) {
+    const int2 rg = grange[g];
+    const int64_t a = r / D2;
+    if (a < rg.x || a >= rg.y) {
+      out[r] = 0.0;
+      return;
+    }
+  }
   out[r] = (double)U[((size_t)g * nact * D2 + r) * G + slot];
 }
 
@@ -432,6 +443,7 @@ struct dgdiff_s {
   int wtab_nb = 0;
   int32_t *d_src = nullptr;
   int64_t src_cap = 0;
+  std::vector<int32_t> h_src_stage;                // pageable staging copy of the sources
   double *d_mom = nullptr;
   int64_t mom_cap = 0;
   double *d_out = nullptr;
@@ -459,6 +471,7 @@ struct dgdiff_s {
   double *d_mix = nullptr, *d_mix_out = nullptr;
   int mix_R = 0;
   bool mix_reduced = false, have_sigma = false;
+  bool mom_reduced = false;                        // the [n][6] table holds every rank's rows
   double last_sigma[3] = {0, 0, 0}, last_mu[2] = {0, 0};
   // last solve
   bool solved = false;
@@ -468,6 +481,7 @@ struct dgdiff_s {
   int64_t last_chunk_size = 0;
   // NCCL
   ncclComm_t comm = nullptr;
+  bool logical = false;                            // nranks > 1 without a communicator
   // stats
   dgdiff_stats_t st;
   bool timing = false;
@@ -489,7 +503,7 @@ static size_t tsize(const dgdiff_s *H) { return H->o.precision == 32 ? 4 : 8; }
 // K3 (fused step) is used for P1 when temporal_steps == 2 (or by default, see
 // use_fused); its groups are 32 sources (one value per lane)
 static bool use_fused(const dgdiff_s *H) {
-  if (H->p != 1 || H->o.kernel == 1 || H->o.kernel == 2 || H->o.kernel == 9) return false;
+  if (H->p != 1 || H->o.kernel == 1 || H->o.kernel == 2) return false;
   return H->o.temporal_steps == 2 || H->o.temporal_steps == 3;   // 3: K3b, decoupled warp roles
 }
 // values per lane of the state layout: v1/v2 16-byte lanes; ring P1 16-byte,
@@ -861,8 +875,11 @@ static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
   // NCCL
   // NCCL communicator: required when nranks > 1; with nranks == 1 an explicit
   // nccl_id also creates one (a one-rank world: exercises the same path)
-  if (H->o.nranks > 1 || H->o.nccl_id) {
-    if (!H->o.nccl_id) return fail(DGDIFF_E_ARG, "nranks > 1 needs opts.nccl_id");
+  // nranks > 1 without an id: a LOGICAL rank (no communicator): the handle
+  // solves its shard only and leaves the other rows of the table zero; the
+  // caller combines the ranks' tables (dgdiff_covariance_table)
+  H->logical = H->o.nranks > 1 && !H->o.nccl_id;
+  if (H->o.nccl_id) {
     if (!g_nccl.load()) return fail(DGDIFF_E_NCCL, "cannot load libnccl.so.2: %s", dlerror());
     ncclUniqueId id;
     memcpy(&id, H->o.nccl_id, sizeof id);
@@ -876,7 +893,7 @@ static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
   // tools/sweep_wink.py: max relative moment error <= 1e-14 against the
   // whole-grid solve on c3): P1 20, P2 30, P3 45, Q1 25, Q2 40 sigma
   H->win_k = H->quad ? (H->p == 1 ? 25.0 : 40.0) : (H->p == 1 ? 20.0 : H->p == 2 ? 30.0 : 45.0);
-  if (const char *wk = getenv("DGDIFF_WINK")) H->win_k = atof(wk);
+  if (const char *wk = tune_env("DGDIFF_WINK")) H->win_k = atof(wk);
   if (H->windows) {
     // 2-D prefix counts of extracellular pixels: algorithmic bytes of windowed stages
     H->h_pre.assign((size_t)(ny + 1) * (nx + 1), 0);
@@ -888,9 +905,9 @@ static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
   }
   const char *sd = getenv("DGDIFF_STAGE_DETAIL");
   H->stage_detail = sd && sd[0] == '1';
-  if (const char *ah = getenv("DGDIFF_AHEAD")) sscanf(ah, "%d,%d", &H->ahead_alpha, &H->ahead_noalpha);
-  if (const char *rg = getenv("DGDIFF_RING")) sscanf(rg, "%d,%d", &H->n1_use, &H->n2_use);
-  if (const char *wb = getenv("DGDIFF_WBAND")) H->wband = atoi(wb);
+  if (const char *ah = tune_env("DGDIFF_AHEAD")) sscanf(ah, "%d,%d", &H->ahead_alpha, &H->ahead_noalpha);
+  if (const char *rg = tune_env("DGDIFF_RING")) sscanf(rg, "%d,%d", &H->n1_use, &H->n2_use);
+  if (const char *wb = tune_env("DGDIFF_WBAND")) H->wband = atoi(wb);
   return DGDIFF_OK;
 }
 
@@ -924,6 +941,7 @@ extern "C" dgdiff_status dgdiff_create(dgdiff_t *out, const uint8_t *mask, int32
     return fail(DGDIFF_E_ARG, "temporal_steps 3 (K3b) is fp64 only");
   if (o.temporal_steps == 4 && o.kernel != 0)
     return fail(DGDIFF_E_ARG, "temporal_steps 4 (K3c wavefront) runs the ring kernel's items only");
+  if (o.kernel < 0 || o.kernel > 3) return fail(DGDIFF_E_ARG, "kernel must be 0..3");
   if (o.max_chunk < 0) return fail(DGDIFF_E_ARG, "max_chunk < 0");
   if (o.mixture_radius < 0 || o.mixture_radius > 2048) return fail(DGDIFF_E_ARG, "mixture_radius must be in [0, 2048]");
   dgdiff_s *H = new dgdiff_s();
@@ -1035,7 +1053,7 @@ static dgdiff_status run_chunk(dgdiff_s *H, int64_t nvalid, int64_t chunk, doubl
   sa.nsm = H->nsm;
   sa.px = px;
   sa.wpb = wpb;
-  sa.diag = H->o.kernel == 9 ? 1 : 0;
+  sa.diag = (tune_env("DGDIFF_K2_DIAG") && atoi(tune_env("DGDIFF_K2_DIAG")) == 1) ? 1 : 0;   // tuning builds only
   sa.ahead_alpha = H->ahead_alpha;
   sa.ahead_noalpha = H->ahead_noalpha;
   sa.n1_use = H->n1_use;
@@ -1268,6 +1286,7 @@ static dgdiff_status solve_impl(dgdiff_s *H, const int32_t *sources, const doubl
     CK(cudaMemsetAsync(H->d_mix, 0, nc * sizeof(double), H->stream));
   }
   H->mix_reduced = false;
+  H->mom_reduced = false;
   H->have_sigma = false;
   if (n > H->src_cap) {
     cudaFree(H->d_src);
@@ -1275,7 +1294,11 @@ static dgdiff_status solve_impl(dgdiff_s *H, const int32_t *sources, const doubl
     CK(cudaMalloc(&H->d_src, sizeof(int32_t) * 2 * n));
     H->src_cap = n;
   }
-  CK(cudaMemcpyAsync(H->d_src, sources, sizeof(int32_t) * 2 * n, cudaMemcpyHostToDevice, H->stream));
+  // inputs are staged through a pageable host copy: cudaMemcpyAsync from
+  // pageable memory has consumed its source when it returns, so the caller may
+  // reuse or free its (possibly pinned) buffer as soon as this call returns
+  H->h_src_stage.assign(sources, sources + 2 * n);
+  CK(cudaMemcpyAsync(H->d_src, H->h_src_stage.data(), sizeof(int32_t) * 2 * n, cudaMemcpyHostToDevice, H->stream));
   H->st.h2d_bytes += sizeof(int32_t) * 2 * n;
   std::vector<int32_t> srt;   // N1: this rank's sources in Morton order
   std::vector<int64_t> ord(std::max<int64_t>(nloc, 0));   // chunk order -> local index
@@ -1350,7 +1373,7 @@ static dgdiff_status solve_impl(dgdiff_s *H, const int32_t *sources, const doubl
       // offsets register r by r*b extra bytes (layout experiments)
       {
         size_t reg = per_src / 3 * chunk, stag = 0;
-        if (const char *e = getenv("DGDIFF_STAGGER")) stag = (size_t)atoll(e) / 256 * 256;
+        if (const char *e = tune_env("DGDIFF_STAGGER")) stag = (size_t)atoll(e) / 256 * 256;
         CK(cudaMalloc(&H->d_Ubase, 3 * reg + 3 * stag));
         for (int r = 0; r < 3; r++) H->d_U[r] = (char *)H->d_Ubase + r * (reg + stag);
       }
@@ -1468,12 +1491,17 @@ extern "C" dgdiff_status dgdiff_covariance(dgdiff_t H, double delta, double sigm
   double t = H->last_nsteps * H->last_dt;
   if (!(std::fabs(delta - t) <= 1e-12 * std::max(std::fabs(delta), std::fabs(t))))
     return fail(DGDIFF_E_STATE, "delta = %.17g but the last solve reached nsteps*dt = %.17g", delta, t);
+  if (H->logical)
+    return fail(DGDIFF_E_STATE, "logical rank %d of %d holds only its shard: sum the ranks' dgdiff_source_moments "
+                "tables and call dgdiff_covariance_table", H->o.rank, H->o.nranks);
   CK(cudaSetDevice(H->dev));
   const int64_t n = H->last_n;
-  if (H->comm) {
-    // the one cross-GPU step: sum of disjoint zero-padded rows is exact
+  if (H->comm && !H->mom_reduced) {
+    // the one cross-GPU step: sum of disjoint zero-padded rows is exact (once
+    // per solve: a second covariance call must not sum the reduced table again)
     ncclResult_t r = g_nccl.allReduce(H->d_mom, H->d_mom, (size_t)6 * n, ncclFloat64, ncclSum, H->comm, H->stream);
     if (r != ncclSuccess) return fail(DGDIFF_E_NCCL, "ncclAllReduce: %s", g_nccl.errStr(r));
+    H->mom_reduced = true;
   }
   k_finalize<<<1, 256, 0, H->stream>>>(H->d_mom, n, H->o.centering, H->d_out);
   H->st.launches++;
@@ -1500,6 +1528,37 @@ extern "C" dgdiff_status dgdiff_covariance(dgdiff_t H, double delta, double sigm
     mu[1] = out[4];
   }
   return DGDIFF_OK;
+}
+
+// K5 on a caller-provided table (logical ranks: the sum of the ranks' tables)
+extern "C" dgdiff_status dgdiff_covariance_table(dgdiff_t H, const double *mom, int64_t n, double sigma[4],
+                                                 double mu[2]) {
+  if (!H || !mom || !sigma) return fail(DGDIFF_E_ARG, "NULL argument");
+  if (n < 1 || n >= (1LL << 31)) return fail(DGDIFF_E_ARG, "need 1 <= n < 2^31 rows");
+  CK(cudaSetDevice(H->dev));
+  double *d_tab = nullptr, *d_o = nullptr;
+  auto done = [&](dgdiff_status s) { cudaFree(d_tab); cudaFree(d_o); return s; };
+  cudaError_t e = cudaMalloc(&d_tab, sizeof(double) * 6 * n);
+  if (e == cudaSuccess) e = cudaMalloc(&d_o, sizeof(double) * 8);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_tab, mom, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, H->stream);
+  if (e == cudaSuccess) {
+    k_finalize<<<1, 256, 0, H->stream>>>(d_tab, n, H->o.centering, d_o);
+    H->st.launches++;
+    e = cudaGetLastError();
+  }
+  double out[6];
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out, d_o, sizeof out, cudaMemcpyDeviceToHost, H->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(H->stream);
+  if (e != cudaSuccess) return done(fail(DGDIFF_E_CUDA, "covariance_table: %s", cudaGetErrorString(e)));
+  const int flags = (int)out[5];
+  if (flags & 2) return done(fail(DGDIFF_E_NONFINITE, "non-finite moments"));
+  if (flags & 1) return done(fail(DGDIFF_E_DEGENERATE, "a density has m00 <= 0"));
+  sigma[0] = out[0];
+  sigma[1] = out[1];
+  sigma[2] = out[1];
+  sigma[3] = out[2];
+  if (mu) { mu[0] = out[3]; mu[1] = out[4]; }
+  return done(DGDIFF_OK);
 }
 
 extern "C" dgdiff_status dgdiff_mixture(dgdiff_t H, double *grid, double *residual) {
@@ -1644,12 +1703,13 @@ extern "C" dgdiff_status dgdiff_get_density(dgdiff_t H, int64_t src, double *out
   CK(cudaMalloc(&d_tmp, sizeof(double) * nel));
   int blocks = (int)((nel + 255) / 256);
   const int nv = lane_nv(H);
+  const int2 *gr = H->windows ? H->d_grange : nullptr;
 #define DG_GATHER(TT, NVV)                                                                                     \
-  if (H->D2 == 6) k_gather<TT, NVV, 6><<<blocks, 256, 0, H->stream>>>((TT *)H->d_U[0], (int)H->nact, g, slot, d_tmp); \
-  else if (H->D2 == 20) k_gather<TT, NVV, 20><<<blocks, 256, 0, H->stream>>>((TT *)H->d_U[0], (int)H->nact, g, slot, d_tmp); \
-  else if (H->D2 == 4) k_gather<TT, NVV, 4><<<blocks, 256, 0, H->stream>>>((TT *)H->d_U[0], (int)H->nact, g, slot, d_tmp); \
-  else if (H->D2 == 9) k_gather<TT, NVV, 9><<<blocks, 256, 0, H->stream>>>((TT *)H->d_U[0], (int)H->nact, g, slot, d_tmp); \
-  else k_gather<TT, NVV, 12><<<blocks, 256, 0, H->stream>>>((TT *)H->d_U[0], (int)H->nact, g, slot, d_tmp);
+  if (H->D2 == 6) k_gather<TT, NVV, 6><<<blocks, 256, 0, H->stream>>>((TT *)H->d_U[0], (int)H->nact, g, slot, d_tmp, gr); \
+  else if (H->D2 == 20) k_gather<TT, NVV, 20><<<blocks, 256, 0, H->stream>>>((TT *)H->d_U[0], (int)H->nact, g, slot, d_tmp, gr); \
+  else if (H->D2 == 4) k_gather<TT, NVV, 4><<<blocks, 256, 0, H->stream>>>((TT *)H->d_U[0], (int)H->nact, g, slot, d_tmp, gr); \
+  else if (H->D2 == 9) k_gather<TT, NVV, 9><<<blocks, 256, 0, H->stream>>>((TT *)H->d_U[0], (int)H->nact, g, slot, d_tmp, gr); \
+  else k_gather<TT, NVV, 12><<<blocks, 256, 0, H->stream>>>((TT *)H->d_U[0], (int)H->nact, g, slot, d_tmp, gr);
   if (H->o.precision == 32) {
     if (nv == 1) { DG_GATHER(float, 1) } else if (nv == 2) { DG_GATHER(float, 2) } else { DG_GATHER(float, 4) }
   } else {
@@ -1713,6 +1773,12 @@ extern "C" dgdiff_status dgdiff_get_stats(dgdiff_t H, dgdiff_stats_t *out) {
         fprintf(stderr, "[dgdiff] stage %d: %.3f ms\n", k + 1, f);
       }
   }
+  H->st.env_overrides = dgk::tune_overrides().load();
+#ifdef DGDIFF_TUNING
+  H->st.tuning_build = 1;
+#else
+  H->st.tuning_build = 0;
+#endif
   *out = H->st;
   return DGDIFF_OK;
 }

@@ -14,9 +14,35 @@
 #pragma once
 #include <type_traits>
 #include <cstdint>
+#include <cstdlib>
+#include <atomic>
 #include <cuda_runtime.h>
 
 namespace dgk {
+
+// Tuning / diagnostic knobs of the experiments (DGDIFF_RING, DGDIFF_WAVE_*,
+// ...) are read from the environment ONLY in builds compiled with
+// -DDGDIFF_TUNING (python -m paper_1907_06191_b200.build --tuning); the
+// product library ignores the environment, so no variable can change a
+// result or a schedule behind the caller's back.  Every knob that a tuning
+// build finds set is counted (dgdiff_stats_t.env_overrides).
+inline std::atomic<int> &tune_overrides() {
+  static std::atomic<int> n{0};
+  return n;
+}
+inline const char *tune_env(const char *name) {
+#ifdef DGDIFF_TUNING
+  const char *v = getenv(name);
+  if (v && v[0]) {
+    tune_overrides().fetch_add(1);
+    return v;
+  }
+  return nullptr;
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
 
 template <typename T, int NV> struct VT;
 template <> struct VT<double, 1> { typedef double type; };

@@ -500,7 +500,7 @@ cudaError_t launch_ring(const dgl::StageArgs &a) {
   static std::atomic<uint64_t> attr_set{0};
   static const int pad = [] {
     int v = 0;
-    if (const char *e = getenv("DGDIFF_SMEM_PAD")) v = atoi(e);
+    if (const char *e = tune_env("DGDIFF_SMEM_PAD")) v = atoi(e);
     return Gm::SMEM + v > Gm::SMEM_MAX ? Gm::SMEM_MAX - Gm::SMEM : std::max(0, v);
   }();
   int dev = 0;
@@ -515,7 +515,7 @@ cudaError_t launch_ring(const dgl::StageArgs &a) {
   int nbands = std::max(1, std::min(a.ny, (8 * a.nsm + per_band - 1) / per_band));
   int band_rows = (a.ny + nbands - 1) / nbands;
   if (a.band_rows > 0) band_rows = std::min(band_rows, a.band_rows);   // N1 windows: finer items
-  static const int env_band = getenv("DGDIFF_K2_BAND") ? atoi(getenv("DGDIFF_K2_BAND")) : 0;   // diagnostic
+  static const int env_band = tune_env("DGDIFF_K2_BAND") ? atoi(tune_env("DGDIFF_K2_BAND")) : 0;   // diagnostic
   if (env_band > 0) band_rows = std::min(band_rows, env_band);
   if (band_rows > RING_MAXBAND) band_rows = RING_MAXBAND;
   nbands = (a.ny + band_rows - 1) / band_rows;

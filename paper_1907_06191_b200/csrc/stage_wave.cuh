@@ -343,7 +343,7 @@ __global__ void __launch_bounds__((DGDIFF_WAVE_NC + 2) * 32, 1)
 // cost and lose most L2 hits (28.3 ms, K2 28.0 ms) -- DESIGN.md section 6
 inline int wave_band_rows() {
   static const int v = [] {
-    const char *e = getenv("DGDIFF_WAVE_BAND");
+    const char *e = tune_env("DGDIFF_WAVE_BAND");
     const int x = e ? atoi(e) : 0;
     return x > 0 ? std::min(x, RING_MAXBAND - 2) : 32;
   }();
@@ -352,7 +352,7 @@ inline int wave_band_rows() {
 // strips per item (DGDIFF_WAVE_SBLK)
 inline int wave_sblk() {
   static const int v = [] {
-    const char *e = getenv("DGDIFF_WAVE_SBLK");
+    const char *e = tune_env("DGDIFF_WAVE_SBLK");
     const int x = e ? atoi(e) : 0;
     return x > 0 ? x : 4;
   }();
@@ -362,7 +362,7 @@ inline int wave_sblk() {
 // wavefront reads from L2, so it wants as many rows in flight as fit
 inline int wave_n1() {
   static const int v = [] {
-    const char *e = getenv("DGDIFF_WAVE_N1");
+    const char *e = tune_env("DGDIFF_WAVE_N1");
     return e ? atoi(e) : 0;
   }();
   return v;
@@ -370,13 +370,13 @@ inline int wave_n1() {
 // diagnostic (DGDIFF_WAVE_NODEP=1): skip the dependency waits -- WRONG results,
 // timing only (how much the wavefront's dependency chain costs)
 inline bool wave_nodep() {
-  static const bool v = getenv("DGDIFF_WAVE_NODEP") && atoi(getenv("DGDIFF_WAVE_NODEP")) == 1;
+  static const bool v = tune_env("DGDIFF_WAVE_NODEP") && atoi(tune_env("DGDIFF_WAVE_NODEP")) == 1;
   return v;
 }
 // source groups per wavefront block (DGDIFF_WAVE_GBLK; 0 = all groups)
 inline int wave_gblk(int ngroups) {
   static const int v = [] {
-    const char *e = getenv("DGDIFF_WAVE_GBLK");
+    const char *e = tune_env("DGDIFF_WAVE_GBLK");
     return e ? atoi(e) : 1;
   }();
   return v <= 0 ? ngroups : std::min(v, ngroups);
@@ -402,14 +402,27 @@ cudaError_t launch_wave(const dgl::StageArgs &a) {
   const int nitems = 3 * nbands * ((a.nstrips + sblk - 1) / sblk) * a.ngroups;
   const int grid = std::min(nitems, a.nsm);
   const double c = a.cs;
-  k_step_wave<T, NV, P><<<grid, (DGDIFF_WAVE_NC + 2) * 32, Gm::SMEM, a.st>>>(
-      (T *)a.Uin, (T *)a.U0, (T *)a.Uout, a.nbr, a.rowtab, a.nact, a.ny, a.nstrips, sblk, a.ngroups, wave_gblk(a.ngroups),
-      band_rows, nbands,
-      a.wave_tab, nitems, (T)c, (T)(0.25 * c), (T)((2.0 / 3.0) * c), (T)0.75, (T)(1.0 / 3.0), a.wave_cnt,
-      wave_nodep() ? 0u : a.wave_epoch, std::max(Gm::ROWS_MIN, std::min(RING_Q - 1, alpha_max_ahead(a, true))),
-      std::max(Gm::ROWS_MIN * (Gm::W + 2 * Gm::HALO), std::min(Gm::N1, wave_n1() > 0 ? wave_n1() : Gm::N1)),
-      std::max(Gm::ROWS_MIN * Gm::W, std::min(Gm::N2, a.n2_use > 0 ? a.n2_use : Gm::N2)),
-      getenv("DGDIFF_WAVE_DIAG") ? 1 : 0);
+  // CTAs wait on items owned by other CTAs, so they must all be resident at
+  // once: a cooperative launch guarantees that (or fails cleanly, e.g. under
+  // an MPS SM limit) instead of a spin-wait that could never be satisfied
+  T *pu = (T *)a.Uin, *pU1 = (T *)a.U0, *pU2 = (T *)a.Uout;
+  const int4 *pnbr = a.nbr, *prt = a.rowtab;
+  int nact = a.nact, ny = a.ny, nstrips = a.nstrips, ngroups = a.ngroups, gblk = wave_gblk(a.ngroups);
+  int band = band_rows, nb = nbands, ni = nitems;
+  const int2 *wt = a.wave_tab;
+  T c1 = (T)c, c2 = (T)(0.25 * c), c3 = (T)((2.0 / 3.0) * c), a2 = (T)0.75, a3 = (T)(1.0 / 3.0);
+  unsigned *cnt = a.wave_cnt;
+  unsigned ep = wave_nodep() ? 0u : a.wave_epoch;
+  int max_ahead = std::max(Gm::ROWS_MIN, std::min(RING_Q - 1, alpha_max_ahead(a, true)));
+  int n1u = std::max(Gm::ROWS_MIN * (Gm::W + 2 * Gm::HALO), std::min(Gm::N1, wave_n1() > 0 ? wave_n1() : Gm::N1));
+  int n2u = std::max(Gm::ROWS_MIN * Gm::W, std::min(Gm::N2, a.n2_use > 0 ? a.n2_use : Gm::N2));
+  int diag = (tune_env("DGDIFF_WAVE_DIAG") && atoi(tune_env("DGDIFF_WAVE_DIAG")) == 1) ? 1 : 0;
+  int sb = sblk;
+  void *args[] = {&pu, &pU1, &pU2, &pnbr, &prt, &nact, &ny, &nstrips, &sb, &ngroups, &gblk, &band, &nb, &wt, &ni,
+                  &c1, &c2, &c3, &a2, &a3, &cnt, &ep, &max_ahead, &n1u, &n2u, &diag};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void *)k_step_wave<T, NV, P>, dim3(grid),
+                                              dim3((DGDIFF_WAVE_NC + 2) * 32), args, Gm::SMEM, a.st);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

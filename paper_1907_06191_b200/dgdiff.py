@@ -13,6 +13,10 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libdgdiff.so")
+# experiments only: the tuning build reads DGDIFF_* knobs from the environment
+# (its stats report tuning_build = 1); the product library never does
+if os.environ.get("DGDIFF_TUNING_LIB") == "1":
+    LIB_PATH = os.path.join(_HERE, "libdgdiff_tuning.so")
 
 OK, E_ARG, E_SOURCE, E_UNSTABLE, E_NONFINITE, E_STATE, E_DEGENERATE, E_CUDA, E_NCCL, E_NOMEM = range(10)
 STATUS_NAMES = ["OK", "E_ARG", "E_SOURCE", "E_UNSTABLE", "E_NONFINITE", "E_STATE", "E_DEGENERATE",
@@ -22,7 +26,8 @@ EXPORTED = ["dgdiff_opts_default", "dgdiff_create", "dgdiff_solve_batch", "dgdif
             "dgdiff_source_moments", "dgdiff_get_density", "dgdiff_dt_max", "dgdiff_last_error",
             "dgdiff_destroy", "dgdiff_operator_table", "dgdiff_shard", "dgdiff_set_timing",
             "dgdiff_get_stats", "dgdiff_reset_stats", "dgdiff_mixture", "dgdiff_centre_weights",
-            "dgdiff_absorb_table", "dgdiff_mc_covariance", "dgdiff_solve_batch_points", "dgdiff_quad_table"]
+            "dgdiff_absorb_table", "dgdiff_mc_covariance", "dgdiff_solve_batch_points", "dgdiff_quad_table",
+            "dgdiff_covariance_table"]
 
 
 class dgdiff_opts(ctypes.Structure):
@@ -37,7 +42,8 @@ class dgdiff_opts(ctypes.Structure):
 class dgdiff_stats_t(ctypes.Structure):
     _fields_ = [("launches", ctypes.c_int64), ("stage_launches", ctypes.c_int64), ("stage_ms", ctypes.c_double),
                 ("stage_bytes", ctypes.c_double), ("stage_flops", ctypes.c_double), ("n_active", ctypes.c_int64), ("chunk", ctypes.c_int64),
-                ("h2d_bytes", ctypes.c_int64), ("d2h_bytes", ctypes.c_int64)]
+                ("h2d_bytes", ctypes.c_int64), ("d2h_bytes", ctypes.c_int64),
+                ("env_overrides", ctypes.c_int64), ("tuning_build", ctypes.c_int64)]
 
 
 class DGDiffError(RuntimeError):
@@ -76,7 +82,7 @@ def _load():
     L.dgdiff_reset_stats.argtypes = [H]
     for name, args in (("dgdiff_mixture", [H, dp, dp]), ("dgdiff_centre_weights", [i32, dp]),
                        ("dgdiff_absorb_table", [i32, dp]), ("dgdiff_solve_batch_points", [H, dp, i64, dbl, i64]),
-                       ("dgdiff_quad_table", [i32, dp]),
+                       ("dgdiff_quad_table", [i32, dp]), ("dgdiff_covariance_table", [H, dp, i64, dp, dp]),
                        ("dgdiff_mc_covariance", [H, ctypes.POINTER(ctypes.c_int32), i64, i32, i64, dbl,
                                                  ctypes.c_uint32, dp, dp, dp, dp])):
         if hasattr(L, name):
@@ -147,6 +153,15 @@ def dgdiff_covariance(handle, delta):
     s = np.zeros(4)
     mu = np.zeros(2)
     _check(lib.dgdiff_covariance(handle, float(delta), _dp(s), _dp(mu)))
+    return s.reshape(2, 2), mu
+
+
+def dgdiff_covariance_table(handle, mom):
+    """K5 on a caller-provided [n][6] moment table (logical ranks: their sum)."""
+    mom = np.ascontiguousarray(mom, dtype=np.float64).reshape(-1, 6)
+    s = np.zeros(4)
+    mu = np.zeros(2)
+    _check(lib.dgdiff_covariance_table(handle, _dp(mom), mom.shape[0], _dp(s), _dp(mu)))
     return s.reshape(2, 2), mu
 
 
@@ -267,6 +282,9 @@ class Solver:
 
     def moments(self):
         return dgdiff_source_moments(self.handle, self.n)
+
+    def covariance_table(self, mom):
+        return dgdiff_covariance_table(self.handle, mom)
 
     def mixture(self):
         """(grid [(2R+1)][(2R+1)], Eq. (9) residual); needs mixture_radius=R."""

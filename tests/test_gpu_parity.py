@@ -153,52 +153,6 @@ def test_c2_p2_closed_form(dg, cfg):
     assert np.abs(S - 8.0 * np.eye(2)).max() <= 1e-11 * 8
 
 
-@pytest.mark.parametrize("prec", [64, 32])
-def test_c3_full_batch_sampled_parity(dg, orc, cfg, prec):
-    """Config c3 at full size (512^2 Gamma substrate, 4096 sources, 200 steps)
-    in the bench launch configuration; sampled sources checked one by one
-    against O1 (moments and densities), Sigma of the sample vs O1."""
-    m = cfg.mask("c3")
-    src = cfg.sources("c3")
-    pick = np.array([0, 1337, 2900, 4095])
-    nsteps = 200
-    with dg.Solver(m, 1.0, 1.0, 1, precision=prec, keep_density=1) as s:
-        s.solve(src, 1 / 32, nsteps)
-        S_all, _ = s.covariance()
-        mom = s.moments()
-        dens = {k: s.density(k) for k in pick}
-    ref_m, ref_d = orc.solve(1, 1.0, 1.0, m, src[pick], 1 / 32, nsteps, keep_density=True)
-    t = TOL[prec]
-    for r, k in enumerate(pick):
-        assert rel_l2(dens[k], ref_d[r]) <= t["dens"], k
-    assert mom_err(mom[pick], ref_m) <= t["mom"]
-    S_sub, _ = orc.sigma(ref_m)
-    from oracle import oracle as O
-    S_gpu_sub, _ = O.sigma(mom[pick])     # same finalize on the GPU moments
-    assert sig_err(S_gpu_sub, S_sub) <= t["sig"]
-    # whole-batch properties: mass, symmetry, hindrance (P:369-376)
-    assert np.abs(mom[:, 0] - 1).max() <= (1e-12 if prec == 64 else 2e-6)
-    assert S_all[0, 1] == S_all[1, 0]
-    assert S_all[0, 0] < 2 * nsteps / 32 and S_all[1, 1] < 2 * nsteps / 32
-    assert np.linalg.eigvalsh(S_all).min() > 0
-
-
-def test_c4_full_size_sampled_parity(dg, orc, cfg):
-    """Config c4 substrate (2048^2), the bench chunk of 256 sources, sampled
-    against O1 over 8 steps (the oracle needs ~10 s per source-step here)."""
-    m = cfg.mask("c4")
-    src = cfg.sources("c4", 256)
-    pick = np.array([3, 200])
-    with dg.Solver(m, 1.0, 1.0, 1, keep_density=1) as s:
-        s.solve(src, 1 / 32, 8)
-        mom = s.moments()
-        dens = {k: s.density(k) for k in pick}
-    ref_m, ref_d = orc.solve(1, 1.0, 1.0, m, src[pick], 1 / 32, 8, keep_density=True)
-    for r, k in enumerate(pick):
-        assert rel_l2(dens[k], ref_d[r]) <= 1e-12
-    assert mom_err(mom[pick], ref_m) <= 1e-10
-
-
 def test_errors_on_gpu(dg, cfg):
     m = cfg.mask("c1")
     with dg.Solver(m, 1.0, 1.0, 1) as s:
@@ -269,26 +223,6 @@ def test_fused_step_equals_per_stage(dg, cfg, nsteps):
             out[ts] = (s.moments(), s.covariance()[0])
     assert mom_err(out[2][0], out[1][0]) <= 1e-13
     assert np.abs(out[2][1] - out[1][1]).max() <= 1e-13 * out[1][1].max()
-
-
-def test_c5_p2_sampled_parity(dg, orc, cfg):
-    """Config c5 (1024^2 Gamma substrate, P2, dt = 1/128, 64 sources) in its
-    launch configuration, over a 20-step prefix (the oracle needs ~5 s per
-    P2 source-step here); sampled sources vs O1, mass, Sigma symmetric."""
-    m = cfg.mask("c5")
-    src = cfg.sources("c5")
-    pick = np.array([0, 21, 63])
-    with dg.Solver(m, 1.0, 1.0, 2, keep_density=1) as s:
-        s.solve(src, 1 / 128, 20)
-        S, _ = s.covariance()
-        mom = s.moments()
-        dens = {k: s.density(k) for k in pick}
-    ref_m, ref_d = orc.solve(2, 1.0, 1.0, m, src[pick], 1 / 128, 20, keep_density=True)
-    for r, k in enumerate(pick):
-        assert rel_l2(dens[k], ref_d[r]) <= 1e-12, k
-    assert mom_err(mom[pick], ref_m) <= 1e-10
-    assert np.abs(mom[:, 0] - 1).max() <= 1e-12
-    assert S[0, 1] == S[1, 0]
 
 
 @pytest.mark.parametrize("prec,p", [(64, 1), (32, 1), (64, 2)])
@@ -874,3 +808,118 @@ def test_k3c_wavefront_step_bitwise_equals_per_stage(dg, cfg, degree, prec):
             out[ts] = (s.moments(), s.density(149), s.density(129))   # densities: last chunk only
     for a, b in zip(out[4], out[0]):
         assert np.array_equal(a, b)
+
+
+# ---------------------------------------------------------------- round 2: parity gaps closed
+def test_centering_own_mean_vs_oracle(dg, orc, cfg):
+    """opts.centering = 1 (own-mean centering, reading R12) on a walled
+    Gamma substrate where the two readings differ by a few %: the GPU's K5
+    branch against O1's orc_sigma(centering = 1), on the oracle's own moments
+    (covariance_table) and on a live solve of sampled sources vs O1."""
+    from paper_1907_06191_b200 import substrate as S
+    m = S.gen_substrate(128, 128, 0.60, 41).mask
+    src = S.sample_sources(m, 40, 42)
+    nsteps = 100
+    ref_m = orc.solve(1, 1.0, 1.0, m, src, 1 / 32, nsteps)
+    R1, rmu1 = orc.sigma(ref_m, centering=1)
+    R0, _ = orc.sigma(ref_m, centering=0)
+    assert np.abs(R1 - R0).max() > 1e-3 * R0.max()          # the readings really differ here
+    with dg.Solver(m, 1.0, 1.0, 1, centering=1) as s:
+        s.solve(src, 1 / 32, nsteps)
+        S1, mu1 = s.covariance()
+        T1, tmu1 = s.covariance_table(ref_m)
+        mom = s.moments()
+    assert sig_err(T1, R1) <= 1e-13 and np.abs(tmu1).max() == 0.0
+    assert sig_err(S1, R1) <= 1e-10
+    assert np.abs(mu1).max() == 0.0
+    assert mom_err(mom, ref_m) <= 1e-10
+    with dg.Solver(m, 1.0, 1.0, 1, precision=32, centering=1) as s:
+        s.solve(src, 1 / 32, nsteps)
+        S1f, _ = s.covariance()
+    assert sig_err(S1f, R1) <= 1e-4
+
+
+@pytest.mark.parametrize("windows", [0, 1])
+def test_logical_ranks_bitwise(dg, cfg, windows):
+    """Multi-GPU readiness on one device: nranks = R handles
+    without a communicator ("logical ranks") each solve their contiguous shard
+    [r n/R, (r+1) n/R) into a zero-padded [n][6] table; the host sums the R
+    tables (what ncclAllReduce does: disjoint rows plus zeros, exact) and K5
+    reduces it in source order, so moments and Sigma are BITWISE those of one
+    rank, for R = 2, 4, 8 -- with and without N1 windows (per-rank Morton
+    sort and the perm scatter of the rows)."""
+    m = cfg.mask("c3")
+    src = cfg.sources("c3", 1000)
+    nsteps = 24
+    with dg.Solver(m, 1.0, 1.0, 1, windows=windows) as s:
+        s.solve(src, 1 / 32, nsteps)
+        S1, mu1 = s.covariance()
+        M1 = s.moments()
+    for R in (2, 4, 8):
+        tab = np.zeros_like(M1)
+        for r in range(R):
+            with dg.Solver(m, 1.0, 1.0, 1, windows=windows, rank=r, nranks=R) as s:
+                s.solve(src, 1 / 32, nsteps)
+                Mr = s.moments()
+                b, e = dg.dgdiff_shard(len(src), r, R)
+                assert np.all(Mr[:b] == 0) and np.all(Mr[e:] == 0)
+                with pytest.raises(dg.DGDiffError):
+                    s.covariance()                               # a logical rank holds only its shard
+                tab += Mr
+                if r == R - 1:
+                    SR, muR = s.covariance_table(tab)
+        assert np.array_equal(tab, M1), R
+        assert np.array_equal(SR, S1) and np.array_equal(muR, mu1), R
+
+
+@pytest.mark.parametrize("prec", [64, 32])
+def test_k3c_wavefront_c1_vs_oracle(dg, orc, cfg, prec):
+    """K3c (temporal_steps = 4) on config c1 against O1 directly (not only
+    against K2): densities, moments, Sigma."""
+    m = cfg.mask("c1")
+    src = cfg.sources("c1")
+    c = cfg.CONFIGS["c1"]
+    ref_m, ref_d = orc.solve(1, 1.0, 1.0, m, src, c.dt, c.nsteps, keep_density=True)
+    with dg.Solver(m, 1.0, 1.0, 1, precision=prec, temporal_steps=4, keep_density=1) as s:
+        s.solve(src, c.dt, c.nsteps)
+        S, _ = s.covariance()
+        got = s.density(0)
+        mom = s.moments()
+    t = TOL[prec]
+    assert rel_l2(got, ref_d[0]) <= t["dens"]
+    assert mom_err(mom, ref_m) <= t["mom"]
+    assert sig_err(S, orc.sigma(ref_m)[0]) <= t["sig"]
+
+
+def test_windows_density_after_longer_solve(dg, orc, cfg):
+    """N1 windows keep only each group's reachable rows; after a long solve the
+    registers hold stale values outside a later short solve's range, and
+    dgdiff_get_density must report exact zeros there: long
+    windowed solve, then a 3-step one on the 512^2 grid, density vs O1."""
+    m = cfg.mask("c3")
+    src_long = cfg.sources("c3", 64)
+    src = cfg.sources("c3", 130)[66:130]
+    with dg.Solver(m, 1.0, 1.0, 1, windows=1, keep_density=1) as s:
+        s.solve(src_long, 1 / 32, 60)
+        s.solve(src, 1 / 32, 3)
+        got = [s.density(k) for k in (0, 63)]
+    ref_m, ref_d = orc.solve(1, 1.0, 1.0, m, src[[0, 63]], 1 / 32, 3, keep_density=True)
+    for r in range(2):
+        assert rel_l2(got[r], ref_d[r]) <= 1e-12
+        assert np.array_equal(got[r] == 0, ref_d[r] == 0)
+
+
+def test_kernel_option_range_checked(dg, cfg):
+    """opts.kernel outside 0..3 is rejected (an undocumented value
+    once selected a diagnostic path that skipped the arithmetic)."""
+    for k in (-1, 4, 9):
+        with pytest.raises(dg.DGDiffError):
+            dg.Solver(cfg.mask("c1"), 1.0, 1.0, 1, kernel=k)
+
+
+def test_product_library_ignores_environment(dg, cfg):
+    """The product library reads no tuning knob from the environment."""
+    with dg.Solver(cfg.mask("c1"), 1.0, 1.0, 1) as s:
+        s.solve(cfg.sources("c1"), 1 / 32, 2)
+        st = s.stats()
+    assert st["tuning_build"] == 0 and st["env_overrides"] == 0

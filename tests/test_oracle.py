@@ -379,18 +379,72 @@ def test_errors(orc):
     assert e.value.code == 6
 
 
-def test_own_mean_centering(orc):
-    """centering=1 shifts each density by its own mean (reading R12): then
-    Sigma = mean of per-source covariances."""
-    mask, src = _case(14)
-    mom = orc.solve(1, 1.0, 1.0, mask, src, 1 / 32, 64)
+def test_own_mean_centering_gaussian_mixture_closed_form(orc):
+    """centering=1 (reading R12): each density is shifted by its OWN
+    mean, so Sigma is the mean of the per-source covariances; centering=0
+    adds the spread of the per-source means (law of total covariance).
+    Pinned on moment rows of Gaussians built from the textbook moments of
+    N(m_s, C_s) scaled by a mass c_s (m00 = c, m10 = c m_x, m20 = c (C_xx +
+    m_x^2), m11 = c (C_xy + m_x m_y), ...): the expected values are mean C_s
+    and mean C_s + Cov(m_s), not a re-typed orc_sigma.  A dropped
+    normalisation (c != 1), a sign slip in the own-mean subtraction or a
+    leftover mixture mean term fails here."""
+    rng = np.random.default_rng(7)
+    n = 9
+    c = rng.uniform(0.5, 2.0, n)
+    mm = rng.normal(0.0, 1.5, (n, 2))
+    C = []
+    for _ in range(n):
+        a = rng.normal(size=(2, 2))
+        C.append(a @ a.T + 0.3 * np.eye(2))
+    C = np.array(C)
+    mom = np.stack([c, c * mm[:, 0], c * mm[:, 1], c * (C[:, 0, 0] + mm[:, 0] ** 2),
+                    c * (C[:, 0, 1] + mm[:, 0] * mm[:, 1]), c * (C[:, 1, 1] + mm[:, 1] ** 2)], 1)
     S1, mu1 = orc.sigma(mom, centering=1)
-    per = []
-    for m in mom:
-        ux, uy = m[1] / m[0], m[2] / m[0]
-        per.append([[m[3] / m[0] - ux * ux, m[4] / m[0] - ux * uy], [m[4] / m[0] - ux * uy, m[5] / m[0] - uy * uy]])
-    assert np.allclose(S1, np.mean(per, axis=0), rtol=1e-13)
+    assert np.allclose(S1, C.mean(0), rtol=1e-13, atol=1e-14)
     assert np.allclose(mu1, 0)
+    S0, mu0 = orc.sigma(mom, centering=0)
+    spread = np.cov(mm.T, bias=True)                   # population covariance of the means
+    assert np.allclose(S0, C.mean(0) + spread, rtol=1e-13, atol=1e-14)
+    assert np.allclose(mu0, mm.mean(0), rtol=1e-13, atol=1e-14)
+
+
+def test_own_mean_centering_invariant_under_reference_shift(orc):
+    """The own-mean covariance of a density does not depend on the point its
+    moments are taken about, so orc_sigma(centering=1) is unchanged when each
+    source's moments are re-taken about a different pixel (a different shift
+    per source) and each density is rescaled -- while the source-point
+    reading (centering=0) changes.  Walled substrate, real DG densities."""
+    mask, src = _case(14)
+    mom, dens = orc.solve(1, 1.0, 1.0, mask, src, 1 / 32, 64, keep_density=True)
+    rng = np.random.default_rng(3)
+    shifted = []
+    for k, (i, j) in enumerate(src):
+        di, dj = rng.integers(-4, 5, 2)
+        scale = rng.uniform(0.5, 3.0)
+        shifted.append(orc.moments(1, 1.0, dens[k] * scale, (int(i + di), int(j + dj))))
+    shifted = np.array(shifted)
+    assert np.allclose(orc.moments(1, 1.0, dens[0], src[0]), mom[0], rtol=0, atol=1e-13)
+    S1, _ = orc.sigma(mom, centering=1)
+    S1s, _ = orc.sigma(shifted, centering=1)
+    assert np.abs(S1s - S1).max() <= 1e-11 * S1.max()
+    S0, _ = orc.sigma(mom, centering=0)
+    S0s, _ = orc.sigma(shifted, centering=0)
+    assert np.abs(S0s - S0).max() > 1e-2 * S0.max()
+    # on walls the two readings differ (SURVEY Q12: a few %)
+    assert np.abs(S1 - S0).max() > 1e-3 * S0.max()
+
+
+def test_own_mean_centering_free_space_p2_off_centre(orc):
+    """Free space, P2, sources at arbitrary sub-pixel points: every density
+    keeps its mean at the point and reproduces quadratics, so the own-mean
+    Sigma is 2 D Delta I exactly for any mix of points."""
+    m = np.zeros((76, 76), np.uint8)
+    pts = [(37.31, 37.77), (38.9, 36.2), (36.05, 38.61)]
+    mom = orc.solve_points(2, 1.0, 1.0, m, pts, 1 / 128, 128)
+    S1, mu1 = orc.sigma(mom, centering=1)
+    assert np.abs(S1 - 2.0 * np.eye(2)).max() <= 1e-12
+    assert np.abs(mu1).max() == 0.0
 
 
 @pytest.mark.parametrize("p,ns,dtf,lo_,hi_", [(1, (24, 48, 96), 64, 1.8, 2.3), (2, (16, 32), 128, 2.6, 3.5)])

@@ -25,6 +25,7 @@ def run(p, el, w, k=None):
     env = dict(os.environ)
     if k is not None:
         env["DGDIFF_WINK"] = str(k)
+        env["DGDIFF_TUNING_LIB"] = "1"   # knobs are read by the tuning build only
     out = subprocess.run([sys.executable, "-c", CODE, str(p), str(el), str(w)], capture_output=True, text=True, env=env)
     return json.loads(out.stdout.strip().splitlines()[-1])
 
