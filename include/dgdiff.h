@@ -67,9 +67,13 @@ typedef struct {
                              one launch per step, the K2 items of all three
                              stages ordered as a skewed wavefront with
                              per-item completion counters; P1/P2 triangles,
+                             fp64/fp32, bit-identical to K2); 5 = stage pair
+                             (K3d: stage 1 on K2, stages 2 and 3 fused in one
+                             launch with U2 kept in shared memory: 5 state
+                             passes per step instead of 8; P1/P2 triangles,
                              fp64/fp32, bit-identical to K2).  Other degrees /
-                             elements use K2; 2..4 exclude ABSORB, windows,
-                             quads, P3; 4 needs kernel 0 */
+                             elements use K2; 2..5 exclude ABSORB, windows,
+                             quads, P3; 4 and 5 need kernel 0 */
   int32_t device;         /* CUDA device ordinal; -1 = current device */
   int32_t rank, nranks;   /* source sharding: rank takes the contiguous block
                              [rank*n/nranks, (rank+1)*n/nranks) of every batch */

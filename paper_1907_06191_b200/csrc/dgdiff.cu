@@ -413,6 +413,8 @@ struct dgdiff_s {
   int4 *d_rowtab = nullptr;  // [nstrips][ny] {h0, c0, c1, h1} for the ring kernel
   int4 *d_rowtab3 = nullptr; // [nstrips3][ny][2] u/U1/U2/output bounds for the fused step
   int4 *d_rowtab_na = nullptr; // ring row table of the stage without the alpha term
+  int4 *d_rowtab_pair = nullptr; // K3d (fused stages 2+3): [nstrips_pair][ny][2]
+  int nstrips_pair = 0;
   int nstrips_na = 0;
   int nstrips3 = 0;
   double macs_per_stage = 0; // structural MACs of one stage over all active pixels (per source)
@@ -582,6 +584,7 @@ static void release(dgdiff_s *H) {
   cudaFree(H->d_rowtab);
   cudaFree(H->d_rowtab3);
   cudaFree(H->d_rowtab_na);
+  cudaFree(H->d_rowtab_pair);
   cudaFree(H->d_pix);
   cudaFree(H->d_aidx);
   cudaFree(H->d_A);
@@ -791,6 +794,32 @@ static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
     CK(cudaMalloc(&H->d_rowtab3, sizeof(int4) * rt3.size()));
     CK(cudaMemcpy(H->d_rowtab3, rt3.data(), sizeof(int4) * rt3.size(), cudaMemcpyHostToDevice));
   }
+  // K3d row table (P1 / P2 triangles): per (strip of W, row) the active-index
+  // bounds of the U1 tile [x0-2, x0+W+2), the U2 pixels [x0-1, x0+W+1) and the
+  // output pixels [x0, x0+W)
+  if (!H->quad && H->p <= 2) {
+    const int W = dgl::pair_width();
+    H->nstrips_pair = (nx + W - 1) / W;
+    std::vector<int> cum((size_t)ny * (nx + 1));
+    int run = 0;
+    for (int j = 0; j < ny; j++) {
+      for (int i = 0; i < nx; i++) {
+        cum[(size_t)j * (nx + 1) + i] = run;
+        if (!mask[(size_t)j * nx + i]) run++;
+      }
+      cum[(size_t)j * (nx + 1) + nx] = run;
+    }
+    std::vector<int4> rp((size_t)H->nstrips_pair * ny * 2);
+    for (int s = 0; s < H->nstrips_pair; s++)
+      for (int j = 0; j < ny; j++) {
+        const int x0 = s * W;
+        auto c = [&](int x) { return cum[(size_t)j * (nx + 1) + std::max(0, std::min(nx, x))]; };
+        rp[((size_t)s * ny + j) * 2] = make_int4(c(x0 - 2), c(x0 - 1), c(x0 + W + 1), c(x0 + W + 2));
+        rp[((size_t)s * ny + j) * 2 + 1] = make_int4(c(x0), c(x0 + W), 0, 0);
+      }
+    CK(cudaMalloc(&H->d_rowtab_pair, sizeof(int4) * rp.size()));
+    CK(cudaMemcpy(H->d_rowtab_pair, rp.data(), sizeof(int4) * rp.size(), cudaMemcpyHostToDevice));
+  }
   H->nsm = prop.multiProcessorCount;
   const std::vector<int4> &nbr_dev = H->quad ? nbr_q : nbr;
   CK(cudaMalloc(&H->d_nbr, sizeof(int4) * nbr_dev.size()));
@@ -936,7 +965,9 @@ extern "C" dgdiff_status dgdiff_create(dgdiff_t *out, const uint8_t *mask, int32
   if (o.element == 1 && (degree > 2 || o.kernel == 1 || o.kernel == 2 || o.temporal_steps >= 2))
     return fail(DGDIFF_E_ARG, "quadrilateral Q_p (N4): degree 1 or 2, default ring kernel only");
   if (o.nranks < 1 || o.rank < 0 || o.rank >= o.nranks) return fail(DGDIFF_E_ARG, "bad rank/nranks");
-  if (o.temporal_steps < 0 || o.temporal_steps > 4) return fail(DGDIFF_E_ARG, "temporal_steps must be 0..4");
+  if (o.temporal_steps < 0 || o.temporal_steps > 5) return fail(DGDIFF_E_ARG, "temporal_steps must be 0..5");
+  if (o.temporal_steps == 5 && (degree > 2 || o.element != 0 || o.kernel != 0 || o.outer_bc != 0 || o.windows != 0))
+    return fail(DGDIFF_E_ARG, "temporal_steps 5 (K3d, fused stages 2+3): P1/P2 triangles, REFLECT, ring kernel, no windows");
   if (o.temporal_steps == 3 && o.precision != 64)
     return fail(DGDIFF_E_ARG, "temporal_steps 3 (K3b) is fp64 only");
   if (o.temporal_steps == 4 && o.kernel != 0)
@@ -1117,6 +1148,38 @@ static dgdiff_status run_chunk(dgdiff_s *H, int64_t nvalid, int64_t chunk, doubl
     H->st.launches += nsteps;
     H->st.stage_launches += nsteps;
     H->st.stage_bytes += 2.0 * pass * nsteps;
+    H->st.stage_flops += fused_flops_per_step(H, chunk) * nsteps;
+    goto after_stepping;
+  }
+  if (H->o.temporal_steps == 5) {
+    // K3d: stage 1 on K2 (u -> Ua), stages 2 + 3 fused in one launch (Ua, u ->
+    // Ub).  u' lands in another register than u (neighbouring strips read u in
+    // their halo columns), so u and Ub trade places after every step.
+    T *cu = u, *cb = Ub;
+    dgl::StageArgs sp = sa;
+    sp.rowtab = H->d_rowtab_pair;
+    sp.nstrips = H->nstrips_pair;
+    sp.cs = c;
+    for (int64_t s = 0; s < nsteps; s++) {
+      cur_step = s;
+      dgdiff_status r;
+      if ((r = stage(0, cu, Ua, 0.0, c)) != DGDIFF_OK) return r;
+      sp.Uin = Ua;
+      sp.U0 = cu;
+      sp.Uout = cb;
+      cudaError_t e = dgl::launch_pair(prec, P, sp);
+      if (e != cudaSuccess) return fail(DGDIFF_E_CUDA, "stage-pair launch: %s", cudaGetErrorString(e));
+      std::swap(cu, cb);
+    }
+    if (cu != u) std::swap(H->d_U[0], H->d_U[2]);   // the final state is always register 0
+    u = (T *)H->d_U[0];
+    if (e1) {
+      CK(cudaEventRecord(e1, st));
+      H->ev_launches_pending += 2 * nsteps;
+    }
+    H->st.launches += 2 * nsteps;
+    H->st.stage_launches += 2 * nsteps;
+    H->st.stage_bytes += 5.0 * pass * nsteps;   // stage 1: u in, U1 out; pair: U1, u in, u' out
     H->st.stage_flops += fused_flops_per_step(H, chunk) * nsteps;
     goto after_stepping;
   }

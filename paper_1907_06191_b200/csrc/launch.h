@@ -53,6 +53,12 @@ cudaError_t launch_dec_f64(const StageArgs &a);
 cudaError_t launch_wave(int prec, int P, const StageArgs &a);
 int wave_band_rows();
 
+// K3d: SSP-RK3 stages 2 and 3 fused in one launch (temporal_steps = 5; P1/P2
+// triangles, REFLECT): a.Uin = U1, a.U0 = u (read only), a.Uout = u' (must not
+// alias u), a.rowtab = the pair row table [nstrips][ny][2] of strips pair_width()
+cudaError_t launch_pair(int prec, int P, const StageArgs &a);
+int pair_width();
+
 // per-TU entry points
 cudaError_t launch_v12_f64(int which, int P, bool alpha, const StageArgs &a);
 cudaError_t launch_v12_f32(int which, int P, bool alpha, const StageArgs &a);

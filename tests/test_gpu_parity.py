@@ -923,3 +923,58 @@ def test_product_library_ignores_environment(dg, cfg):
         s.solve(cfg.sources("c1"), 1 / 32, 2)
         st = s.stats()
     assert st["tuning_build"] == 0 and st["env_overrides"] == 0
+
+
+# ---------------------------------------------------------------- K3d: fused stages 2 + 3
+@pytest.mark.parametrize("degree,prec", [(1, 64), (1, 32), (2, 64), (2, 32)])
+def test_k3d_stage_pair_bitwise_equals_per_stage(dg, cfg, degree, prec):
+    """K3d (temporal_steps = 5: stage 1 on K2, stages 2 + 3 in one launch with
+    U2 in shared memory) does each pixel's arithmetic exactly as K2: moments
+    and densities bit-identical on the c3 substrate (64 strips of 8 columns,
+    several bands, two source groups and a ragged second chunk), over an even
+    and an odd number of steps (the u / u' registers trade places each step)."""
+    m = cfg.mask("c3")
+    G = {(1, 64): 64, (1, 32): 128, (2, 64): 32, (2, 32): 64}[(degree, prec)]
+    src = cfg.sources("c3", 400)[:2 * G + 7]
+    dt = 1 / 32 if degree == 1 else 1 / 128
+    for nsteps in (4, 5):
+        out = {}
+        for ts in (0, 5):
+            with dg.Solver(m, 1.0, 1.0, degree, precision=prec, temporal_steps=ts, keep_density=1,
+                           max_chunk=2 * G) as s:
+                s.solve(src, dt, nsteps)
+                S, mu = s.covariance()
+                n = len(src)
+                out[ts] = (s.moments(), S, mu, s.density(n - 1), s.density(2 * G))
+        for a, b in zip(out[5], out[0]):
+            assert np.array_equal(a, b), (degree, prec, nsteps)
+
+
+@pytest.mark.parametrize("prec", [64, 32])
+def test_k3d_c1_and_random_masks_vs_oracle(dg, orc, cfg, prec):
+    """K3d against O1 directly: config c1 (full density, 200 steps) and a
+    random mask with every face code, walls on the grid edge and a ragged
+    batch (P1 and P2)."""
+    m = cfg.mask("c1")
+    c = cfg.CONFIGS["c1"]
+    ref_m, ref_d = orc.solve(1, 1.0, 1.0, m, cfg.sources("c1"), c.dt, c.nsteps, keep_density=True)
+    with dg.Solver(m, 1.0, 1.0, 1, precision=prec, temporal_steps=5, keep_density=1) as s:
+        s.solve(cfg.sources("c1"), c.dt, c.nsteps)
+        S, _ = s.covariance()
+        got = s.density(0)
+    t = TOL[prec]
+    assert rel_l2(got, ref_d[0]) <= t["dens"]
+    assert sig_err(S, orc.sigma(ref_m)[0]) <= t["sig"]
+    rng = np.random.default_rng(77)
+    mm = (rng.random((21, 37)) < 0.4).astype(np.uint8)
+    free = np.argwhere(mm == 0)
+    src = free[rng.integers(0, len(free), 45)][:, ::-1].astype(np.int32)
+    for p in (1, 2):
+        dt = (1 / 32 if p == 1 else 1 / 128)
+        rm, rd = orc.solve(p, 1.0, 1.0, mm, src, dt, 13, keep_density=True)
+        with dg.Solver(mm, 1.0, 1.0, p, precision=prec, temporal_steps=5, keep_density=1) as s:
+            s.solve(src, dt, 13)
+            mom = s.moments()
+            for k in (0, 44):
+                assert rel_l2(s.density(k), rd[k]) <= t["dens"], (p, k)
+        assert mom_err(mom, rm) <= t["mom"], p
