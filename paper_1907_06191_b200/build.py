@@ -76,6 +76,8 @@ def _compile(src, verbose, tuning=False):
         cmd.insert(1, "-Xptxas=-v")
     if tuning:
         cmd.insert(1, "-DDGDIFF_TUNING")
+        for f in os.environ.get("DGDIFF_TUNING_FLAGS", "").split():   # e.g. -DDGDIFF_PAIR_W=6
+            cmd.insert(1, f)
     r = subprocess.run(cmd, capture_output=True, text=True)
     if verbose or r.returncode:
         sys.stderr.write(r.stdout + r.stderr)

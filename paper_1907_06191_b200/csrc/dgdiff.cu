@@ -415,6 +415,7 @@ struct dgdiff_s {
   int4 *d_rowtab_na = nullptr; // ring row table of the stage without the alpha term
   int4 *d_rowtab_pair = nullptr; // K3d (fused stages 2+3): [nstrips_pair][ny][2]
   int nstrips_pair = 0;
+  uint16_t *d_nbs_pair = nullptr;  // K3d strip-major neighbour table
   int nstrips_na = 0;
   int nstrips3 = 0;
   double macs_per_stage = 0; // structural MACs of one stage over all active pixels (per source)
@@ -585,6 +586,7 @@ static void release(dgdiff_s *H) {
   cudaFree(H->d_rowtab3);
   cudaFree(H->d_rowtab_na);
   cudaFree(H->d_rowtab_pair);
+  cudaFree(H->d_nbs_pair);
   cudaFree(H->d_pix);
   cudaFree(H->d_aidx);
   cudaFree(H->d_A);
@@ -809,16 +811,34 @@ static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
       }
       cum[(size_t)j * (nx + 1) + nx] = run;
     }
+    // and the strip-major 16-bit neighbour table of the U2 pixels: open-face
+    // code (bits 0-3), the N / S neighbours' positions in the tiles of rows
+    // j+1 / j-1 (bits 4-7 / 8-11, counted from column x0-2); rowtab .z of
+    // the second int4 = the (strip, row)'s first entry
     std::vector<int4> rp((size_t)H->nstrips_pair * ny * 2);
+    std::vector<uint16_t> nbs;
+    nbs.reserve((size_t)H->nact * (W + 2) / W + 64);
+    auto act = [&](int i, int j) { return i >= 0 && j >= 0 && i < nx && j < ny && !mask[(size_t)j * nx + i]; };
     for (int s = 0; s < H->nstrips_pair; s++)
       for (int j = 0; j < ny; j++) {
         const int x0 = s * W;
-        auto c = [&](int x) { return cum[(size_t)j * (nx + 1) + std::max(0, std::min(nx, x))]; };
+        auto cr = [&](int jj, int x) { return cum[(size_t)jj * (nx + 1) + std::max(0, std::min(nx, x))]; };
+        auto c = [&](int x) { return cr(j, x); };
         rp[((size_t)s * ny + j) * 2] = make_int4(c(x0 - 2), c(x0 - 1), c(x0 + W + 1), c(x0 + W + 2));
-        rp[((size_t)s * ny + j) * 2 + 1] = make_int4(c(x0), c(x0 + W), 0, 0);
+        rp[((size_t)s * ny + j) * 2 + 1] = make_int4(c(x0), c(x0 + W), (int)nbs.size(), 0);
+        for (int i = std::max(0, x0 - 1); i < std::min(nx, x0 + W + 1); i++) {
+          if (!act(i, j)) continue;
+          int e = (act(i + 1, j) ? 1 : 0) | (act(i - 1, j) ? 2 : 0) | (act(i, j + 1) ? 4 : 0) | (act(i, j - 1) ? 8 : 0);
+          if (e & 4) e |= (aidx[(size_t)(j + 1) * nx + i] - cr(j + 1, x0 - 2)) << 4;
+          if (e & 8) e |= (aidx[(size_t)(j - 1) * nx + i] - cr(j - 1, x0 - 2)) << 8;
+          nbs.push_back((uint16_t)e);
+        }
       }
+    nbs.resize(nbs.size() + 16, 0);   // the bulk copies round the end up to 16 bytes
     CK(cudaMalloc(&H->d_rowtab_pair, sizeof(int4) * rp.size()));
     CK(cudaMemcpy(H->d_rowtab_pair, rp.data(), sizeof(int4) * rp.size(), cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&H->d_nbs_pair, sizeof(uint16_t) * nbs.size()));
+    CK(cudaMemcpy(H->d_nbs_pair, nbs.data(), sizeof(uint16_t) * nbs.size(), cudaMemcpyHostToDevice));
   }
   H->nsm = prop.multiProcessorCount;
   const std::vector<int4> &nbr_dev = H->quad ? nbr_q : nbr;
@@ -1158,6 +1178,7 @@ static dgdiff_status run_chunk(dgdiff_s *H, int64_t nvalid, int64_t chunk, doubl
     T *cu = u, *cb = Ub;
     dgl::StageArgs sp = sa;
     sp.rowtab = H->d_rowtab_pair;
+    sp.nbs = H->d_nbs_pair;
     sp.nstrips = H->nstrips_pair;
     sp.cs = c;
     for (int64_t s = 0; s < nsteps; s++) {

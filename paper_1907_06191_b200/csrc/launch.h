@@ -32,6 +32,8 @@ struct StageArgs {
   unsigned *wave_cnt = nullptr;
   const int2 *wave_tab = nullptr;
   unsigned wave_epoch = 0;
+  // K3d: strip-major 16-bit neighbour table of the U2 pixels (see stage_pair.cuh)
+  const uint16_t *nbs = nullptr;
   cudaStream_t st = nullptr;
 };
 

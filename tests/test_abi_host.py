@@ -220,9 +220,12 @@ def test_argument_errors_are_reported(dg):
     with pytest.raises(dg.DGDiffError) as e:
         dg.dgdiff_create(np.zeros((4, 4), np.uint8), 1.0, 1.0, 1, dg.dgdiff_opts_default(outer_bc=2))
     assert e.value.status == dg.E_ARG
-    # K3b is fp64 only; K3c (4) needs the ring kernel; temporal_steps in 0..4
-    for bad in (dict(temporal_steps=3, precision=32), dict(temporal_steps=4, kernel=1), dict(temporal_steps=5),
-                dict(temporal_steps=4, outer_bc=1), dict(temporal_steps=4, windows=1)):
+    # K3b is fp64 only; K3c (4) and K3d (5) need the ring kernel and REFLECT;
+    # temporal_steps in 0..5; opts.kernel in 0..3
+    for bad in (dict(temporal_steps=3, precision=32), dict(temporal_steps=4, kernel=1), dict(temporal_steps=6),
+                dict(temporal_steps=4, outer_bc=1), dict(temporal_steps=4, windows=1),
+                dict(temporal_steps=5, kernel=1), dict(temporal_steps=5, outer_bc=1), dict(temporal_steps=5, element=1),
+                dict(kernel=4), dict(kernel=9), dict(kernel=-1)):
         with pytest.raises(dg.DGDiffError) as e:
             dg.dgdiff_create(np.zeros((4, 4), np.uint8), 1.0, 1.0, 1, dg.dgdiff_opts_default(**bad))
         assert e.value.status == dg.E_ARG, bad

@@ -16,6 +16,9 @@ from paper_1907_06191_b200 import configs, dgdiff as dg  # noqa: E402
 tss = [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "0,5").split(",")]
 cases = [("c4", 1, 64, 256, 1 / 32, 8), ("c4", 1, 32, 256, 1 / 32, 8), ("c5", 2, 64, 64, 1 / 128, 40),
          ("c3", 1, 64, 1024, 1 / 32, 16)]
+only = os.environ.get("PAIR_CASES")
+if only:
+    cases = [c for c in cases if f"{c[0]}_p{c[1]}_fp{c[2]}" in only.split(",")]
 for name, deg, prec, n, dt, nsteps in cases:
     m = configs.mask(name)
     src = configs.sources(name, n)
