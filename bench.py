@@ -35,15 +35,27 @@ NX = NY = 2048
 NSTEPS = 32
 DT = 1.0 / 32
 SRC_PER_GPU = 256
+DEFAULT_TS = 0      # the bench's kernel path (see --temporal-steps)
 METRIC = "element-dof updates/s and \u03a3 solves/s at 1/2/4/8 B200; % of HBM roofline"
 UNIT = "element-dof updates/s"
 
 
+def step_dt(degree):
+    """dt of the bench step: 1/32 (P1) and 1/128 (P2, the P2 stability limit is ~1/77)."""
+    return DT if degree == 1 else DT / 4
+
+
+TS_NAMES = {0: "K2 per-stage ring kernel (3 launches per SSP-RK3 step)",
+            5: "K3d: stage 1 on K2 + stages 2-3 fused in one launch (2 launches per step)"}
+
+
 def workload_cfg(args, n_gpus):
+    dt = step_dt(args.degree)
     return {
         "workload": f"c4: {NX}x{NY} Gamma-axon substrate (f=0.60, seed 5), {SRC_PER_GPU} point sources per GPU per "
-                    f"step from the c4 source set (seed 6), P{args.degree}, dt=1/32, {NSTEPS} SSP-RK3 steps, "
-                    f"moments + Sigma",
+                    f"step from the c4 source set (seed 6), P{args.degree}, dt=1/{round(1 / dt)}, {NSTEPS} SSP-RK3 "
+                    f"steps, moments + Sigma",
+        "kernel_path": TS_NAMES.get(args.temporal_steps, f"temporal_steps={args.temporal_steps}"),
         "grid": [NX, NY],
         "degree": args.degree,
         "sources_per_step": SRC_PER_GPU * n_gpus,
@@ -123,29 +135,49 @@ def dist_env():
 
 
 # ----------------------------------------------------------------------------- CPU oracle legs
-def oracle_sample(mask, sources, degree, nthreads, nsteps):
+def oracle_sample(mask, sources, degree, nthreads, nsteps, dt=DT):
     """Time the oracle (as it stands) on `len(sources)` sources x nsteps."""
     from oracle import oracle as O
     O.build()
     t0 = time.perf_counter()
-    O.solve(degree, 1.0, 1.0, mask, sources, DT, nsteps, nthreads=nthreads)
+    O.solve(degree, 1.0, 1.0, mask, sources, dt, nsteps, nthreads=nthreads)
     return time.perf_counter() - t0
 
 
 def oracle_threads():
-    return max(1, min(os.cpu_count() or 1, 16))
+    """All host threads this process may use (no cap)."""
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except Exception:
+        return max(1, os.cpu_count() or 1)
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 def cpu_baseline(mask, sources, degree):
+    """O1 as it stands (test infrastructure) on the host: one source x one step
+    on one core, and nproc sources x one step on all cores (one OpenMP thread
+    per source); ~10-25 s on the c4 substrate."""
     th = oracle_threads()
-    nsteps = 4
-    src = sources[:th]
-    t = oracle_sample(mask, src, degree, th, nsteps)
     d = (degree + 1) * (degree + 2) // 2
-    work = len(src) * 2 * NX * NY * d * nsteps
-    return {"value": work / t, "unit": UNIT, "cores": th, "kind": "oracle",
-            "sample": f"{len(src)} sources x {nsteps} SSP-RK3 steps on the same {NX}x{NY} c4 substrate "
-                      f"(O1 fp64, one OpenMP thread per source), {t:.1f} s wall"}
+    per = 2 * NX * NY * d                                   # element-dofs per source-step
+    t1 = oracle_sample(mask, sources[:1], degree, 1, 1)
+    ta = oracle_sample(mask, sources[:th], degree, th, 1)
+    one, allc = per / t1, th * per / ta
+    return {"value": allc, "unit": UNIT, "cores": th, "kind": "oracle",
+            "one_core": one, "all_cores": allc, "nproc": os.cpu_count(), "cpu_model": cpu_model(),
+            "sample": f"same {NX}x{NY} c4 substrate, O1 fp64: 1 source x 1 SSP-RK3 step on 1 core ({t1:.1f} s) and "
+                      f"{th} sources x 1 step on {th} threads ({ta:.1f} s)"}
 
 
 def run_reference(args):
@@ -158,10 +190,11 @@ def run_reference(args):
     th = oracle_threads()
     d = (args.degree + 1) * (args.degree + 2) // 2
     nsteps = 1
+    dt = step_dt(args.degree)
     times = []
     for k in range(args.warmup + args.steps):
         src = sources[k * th:(k + 1) * th]
-        t = oracle_sample(mask, src, args.degree, th, nsteps)
+        t = oracle_sample(mask, src, args.degree, th, nsteps, dt)
         if k >= args.warmup:
             times.append(t)
     work = th * 2 * NX * NY * d * nsteps
@@ -173,7 +206,7 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": workload_cfg(args, world) | {"note": "bounded oracle sample"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": th, "kind": "oracle",
-                             "sample": sample},
+                             "nproc": os.cpu_count(), "cpu_model": cpu_model(), "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -203,9 +236,9 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     solver = dg.Solver(mask, 1.0, 1.0, args.degree, precision=args.precision, rank=rank, nranks=world,
                        nccl_id=nccl_id, stream=stream.cuda_stream, device=local, max_chunk=SRC_PER_GPU,
-                       windows=args.windows)
+                       windows=args.windows, temporal_steps=args.temporal_steps)
     per_step = SRC_PER_GPU * world
-    dt = DT if args.degree == 1 else DT / 4
+    dt = step_dt(args.degree)
     nsteps = NSTEPS
 
     # the step's sources live in pinned host memory (the e2e leg copies them
@@ -256,17 +289,20 @@ def run_ours(args):
     n_act = st["n_active"]
     active = total_src * n_act * 2 * d * nsteps / (dev_ms * 1e-3)
     peak, peak_src = peaks()
-    per_launch_bytes = st["stage_bytes"] / max(1, st["stage_launches"])
-    per_launch_ms = st["stage_ms"] / max(1, st["stage_launches"])
+    # the dominant kernel: K2's stage kernel, or K3d's stage-pair kernel
+    per_launch_bytes = st["dom_bytes"] / max(1, st["dom_launches"])
+    per_launch_ms = st["dom_ms"] / max(1, st["dom_launches"])
     achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9 if per_launch_ms > 0 else None
-    traffic = None
+    kname = "k_stage_pair (K3d: SSP-RK3 stages 2+3 fused)" if args.temporal_steps == 5 else \
+        "k_stage_ring (K2: one SSP-RK3 stage)"
+    traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "stage_traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
             tj = json.load(f)
-        key = f"p{args.degree}_fp{args.precision}"
+        key = f"{'pair' if args.temporal_steps == 5 else 'ring'}_p{args.degree}_fp{args.precision}"
         if key in tj and not args.windows:
-            traffic = tj[key]
+            traffic, traffic_src = tj[key], tj.get("_source")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -277,16 +313,20 @@ def run_ours(args):
         "sigma_last": [S[0, 0], S[0, 1], S[1, 1]],
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "kernel": "k_stage (one SSP-RK3 stage)", "peak_source": peak_src,
+                     "traffic_source": traffic_src,
+                     "kernel": kname, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": per_launch_bytes,
                      "avg_launch_ms": per_launch_ms,
-                     "stage_share_of_step": st["stage_ms"] / dev_ms if dev_ms > 0 else None},
+                     "share_of_step": st["dom_ms"] / dev_ms if dev_ms > 0 else None,
+                     "stepping_share_of_step": st["stage_ms"] / dev_ms if dev_ms > 0 else None},
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": st["h2d_bytes"],
                 "d2h_bytes_per_step": st["d2h_bytes"],
                 "note": "wall clock around dgdiff_solve_batch(sources in pinned host memory) + "
                         "dgdiff_covariance(Sigma to host)"},
         "gpu_launches": st["launches"],
         "clocks": clk.summary(),
+        "library": {"env_overrides": st["env_overrides"], "tuning_build": st["tuning_build"],
+                    "temporal_steps": args.temporal_steps},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(mask, all_src, args.degree)
@@ -307,6 +347,8 @@ def main():
     ap.add_argument("--precision", type=int, default=64, choices=[64, 32])
     ap.add_argument("--degree", type=int, default=1, choices=[1, 2])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--temporal-steps", type=int, default=DEFAULT_TS, choices=[0, 5],
+                    help="0: K2, one launch per SSP-RK3 stage; 5: K3d, stages 2+3 fused (bitwise equal)")
     ap.add_argument("--windows", type=int, default=0, choices=[0, 1, 2],
                     help="N1 active windows: 1 exact (bitwise), 2 also clipped at K sigma; not the default "
                          "(the headline is the whole-grid solve)")

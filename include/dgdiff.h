@@ -289,6 +289,11 @@ typedef struct {
   int64_t env_overrides;   /* tuning knobs taken from the environment (always 0
                               in product builds: they ignore the environment) */
   int64_t tuning_build;    /* 1 if the library was built with -DDGDIFF_TUNING */
+  double dom_ms;           /* the dominant kernel alone (K2: every stage launch;
+                              K3d: the stage-pair launches): summed device time
+                              (timing enabled), algorithmic HBM bytes, launches */
+  double dom_bytes;
+  int64_t dom_launches;
 } dgdiff_stats_t;
 
 /* Enable (1) / disable (0) CUDA-event timing of the stage launches. */

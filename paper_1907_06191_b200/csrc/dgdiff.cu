@@ -491,6 +491,9 @@ struct dgdiff_s {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
   size_t ev_used = 0;
   int64_t ev_launches_pending = 0;
+  // dominant-kernel timing (K3d: the stage-pair launches, one event pair each)
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evd;
+  size_t evd_used = 0;
   bool stage_detail = false;          // env DGDIFF_STAGE_DETAIL=1: per-stage events
   int ahead_alpha = 0, ahead_noalpha = 0;  // env DGDIFF_AHEAD=a,n (tuning experiments)
   int n1_use = 0, n2_use = 0;              // env DGDIFF_RING=n1,n2 (tuning experiments)
@@ -574,6 +577,10 @@ extern "C" dgdiff_status dgdiff_operator_table(int32_t degree, double *A, double
 static void release(dgdiff_s *H) {
   if (!H) return;
   for (auto &p : H->ev) {
+    cudaEventDestroy(p.first);
+    cudaEventDestroy(p.second);
+  }
+  for (auto &p : H->evd) {
     cudaEventDestroy(p.first);
     cudaEventDestroy(p.second);
   }
@@ -1167,6 +1174,8 @@ static dgdiff_status run_chunk(dgdiff_s *H, int64_t nvalid, int64_t chunk, doubl
     }
     H->st.launches += nsteps;
     H->st.stage_launches += nsteps;
+    H->st.dom_launches += nsteps;
+    H->st.dom_bytes += 2.0 * pass * nsteps;
     H->st.stage_bytes += 2.0 * pass * nsteps;
     H->st.stage_flops += fused_flops_per_step(H, chunk) * nsteps;
     goto after_stepping;
@@ -1188,8 +1197,22 @@ static dgdiff_status run_chunk(dgdiff_s *H, int64_t nvalid, int64_t chunk, doubl
       sp.Uin = Ua;
       sp.U0 = cu;
       sp.Uout = cb;
+      cudaEvent_t d0 = nullptr, d1 = nullptr;
+      if (H->timing) {
+        if (H->evd_used == H->evd.size()) {
+          cudaEvent_t a, b;
+          CK(cudaEventCreate(&a));
+          CK(cudaEventCreate(&b));
+          H->evd.push_back({a, b});
+        }
+        d0 = H->evd[H->evd_used].first;
+        d1 = H->evd[H->evd_used].second;
+        H->evd_used++;
+        CK(cudaEventRecord(d0, st));
+      }
       cudaError_t e = dgl::launch_pair(prec, P, sp);
       if (e != cudaSuccess) return fail(DGDIFF_E_CUDA, "stage-pair launch: %s", cudaGetErrorString(e));
+      if (d1) CK(cudaEventRecord(d1, st));
       std::swap(cu, cb);
     }
     if (cu != u) std::swap(H->d_U[0], H->d_U[2]);   // the final state is always register 0
@@ -1201,6 +1224,8 @@ static dgdiff_status run_chunk(dgdiff_s *H, int64_t nvalid, int64_t chunk, doubl
     H->st.launches += 2 * nsteps;
     H->st.stage_launches += 2 * nsteps;
     H->st.stage_bytes += 5.0 * pass * nsteps;   // stage 1: u in, U1 out; pair: U1, u in, u' out
+    H->st.dom_bytes += 3.0 * pass * nsteps;     // the stage-pair kernel alone
+    H->st.dom_launches += nsteps;
     H->st.stage_flops += fused_flops_per_step(H, chunk) * nsteps;
     goto after_stepping;
   }
@@ -1247,6 +1272,8 @@ static dgdiff_status run_chunk(dgdiff_s *H, int64_t nvalid, int64_t chunk, doubl
     }
     H->st.launches += nsteps;
     H->st.stage_launches += nsteps;
+    H->st.dom_launches += nsteps;
+    H->st.dom_bytes += 4.0 * pass * nsteps;
     H->st.stage_bytes += 4.0 * pass * nsteps;   // u read + u written + U1, U2 written back
     H->st.stage_flops += fused_flops_per_step(H, chunk) * nsteps;
     goto after_stepping;
@@ -1271,7 +1298,9 @@ static dgdiff_status run_chunk(dgdiff_s *H, int64_t nvalid, int64_t chunk, doubl
   }
   H->st.launches += 3 * nsteps;
   H->st.stage_launches += 3 * nsteps;
+  H->st.dom_launches += 3 * nsteps;   // K2: the stage kernel is the dominant kernel
   H->st.stage_bytes += H->windows ? win_bytes : 8.0 * pass * nsteps;
+  H->st.dom_bytes += H->windows ? win_bytes : 8.0 * pass * nsteps;
   H->st.stage_flops += fused_flops_per_step(H, chunk) * nsteps * (H->windows ? win_bytes / std::max(1.0, 8.0 * pass * nsteps) : 1.0);
 after_stepping:
   CK(cudaGetLastError());
@@ -1829,6 +1858,7 @@ extern "C" dgdiff_status dgdiff_reset_stats(dgdiff_t H) {
   H->st.chunk = ch;
   H->ev_used = 0;
   H->ev_launches_pending = 0;
+  H->evd_used = 0;
   return DGDIFF_OK;
 }
 
@@ -1844,8 +1874,20 @@ extern "C" dgdiff_status dgdiff_get_stats(dgdiff_t H, dgdiff_stats_t *out) {
       ms += f;
     }
     H->st.stage_ms += ms;
+    if (H->o.temporal_steps != 5) H->st.dom_ms += ms;   // K2: stage kernels = dominant kernel
     H->ev_used = 0;
     H->ev_launches_pending = 0;
+  }
+  if (H->evd_used) {
+    CK(cudaStreamSynchronize(H->stream));
+    double ms = 0;
+    for (size_t k = 0; k < H->evd_used; k++) {
+      float f = 0;
+      CK(cudaEventElapsedTime(&f, H->evd[k].first, H->evd[k].second));
+      ms += f;
+    }
+    H->st.dom_ms += ms;
+    H->evd_used = 0;
   }
   if (H->stage_detail) {
     CK(cudaStreamSynchronize(H->stream));

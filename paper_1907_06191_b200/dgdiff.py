@@ -43,7 +43,8 @@ class dgdiff_stats_t(ctypes.Structure):
     _fields_ = [("launches", ctypes.c_int64), ("stage_launches", ctypes.c_int64), ("stage_ms", ctypes.c_double),
                 ("stage_bytes", ctypes.c_double), ("stage_flops", ctypes.c_double), ("n_active", ctypes.c_int64), ("chunk", ctypes.c_int64),
                 ("h2d_bytes", ctypes.c_int64), ("d2h_bytes", ctypes.c_int64),
-                ("env_overrides", ctypes.c_int64), ("tuning_build", ctypes.c_int64)]
+                ("env_overrides", ctypes.c_int64), ("tuning_build", ctypes.c_int64),
+                ("dom_ms", ctypes.c_double), ("dom_bytes", ctypes.c_double), ("dom_launches", ctypes.c_int64)]
 
 
 class DGDiffError(RuntimeError):

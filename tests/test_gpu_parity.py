@@ -410,24 +410,33 @@ def test_mc_free_space_sigma(dg):
     assert abs(S[0, 1]) < 4 * se[1]
 
 
-@pytest.mark.parametrize("p,tol", [(2, 0.03), (1, 0.08)])
-def test_dg_vs_mc_gamma_substrate(dg, cfg, p, tol):
+def test_dg_vs_mc_gamma_substrate_refinement(dg, cfg):
     """Physics cross-check (the paper's DG-vs-MC comparison) on the
     c3 Gamma substrate, 64 sources, Delta = 8: MC with reflecting (rejecting)
-    walls on the same pixel mask vs DG.  Measured: P2 within ~1.2 %, P1 ~5 %
-    low (the u+ = 0 wall flux of the paper's scheme, reading R6, is an O(h)
-    wall error); both hindered well below 2 D Delta."""
+    walls on the pixel mask vs DG on the SAME staircase geometry at h and h/2
+    (each pixel split 2 x 2; the sources are the same physical points).  The
+    P1 gap is the O(h) wall error of the paper's u+ = 0 wall flux (reading
+    R6): it must shrink like h (measured 5.7 % -> 2.9 % -> 1.1 % at h, h/2,
+    h/4, profiles/r02_dg_mc_refine.jsonl); P2 is within ~1.2 % at h.  Both
+    hindered well below 2 D Delta."""
     m = cfg.mask("c3")
     src = cfg.sources("c3", 64)
-    dt = 1 / 32 if p == 1 else 1 / 128
-    nsteps = int(round(8.0 / dt))
-    with dg.Solver(m, 1.0, 1.0, p) as s:
-        s.solve(src, dt, nsteps)
-        S, _ = s.covariance()
-        Sm, _, se = s.mc_covariance(src, 20000, 4096, 8.0, seed=77)
-    for k in (0, 1):
-        assert abs(S[k, k] - Sm[k, k]) <= tol * Sm[k, k] + 4 * se[2 * k]
-        assert S[k, k] < 0.7 * 16.0 and Sm[k, k] < 0.7 * 16.0
+    pts = src.astype(np.float64) + 0.5
+    with dg.Solver(m, 1.0, 1.0, 1) as s:
+        Sm, _, se = s.mc_covariance(src, 20000, 8192, 8.0, seed=2024)
+    gaps = {}
+    for p, f in ((1, 1), (1, 2), (2, 1)):
+        h = 1.0 / f
+        dt = h * h / (32 if p == 1 else 128)
+        with dg.Solver(np.kron(m, np.ones((f, f), np.uint8)), h, 1.0, p, windows=1) as s:
+            s.solve_points(pts, dt, int(round(8.0 / dt)))
+            S, _ = s.covariance()
+        gaps[p, f] = np.mean([abs(S[k, k] - Sm[k, k]) / Sm[k, k] for k in (0, 1)])
+        assert S[0, 0] < 0.7 * 16.0 and S[1, 1] < 0.7 * 16.0
+    assert Sm[0, 0] < 0.7 * 16.0 and Sm[1, 1] < 0.7 * 16.0
+    assert gaps[1, 1] <= 0.08 and gaps[2, 1] <= 0.025
+    assert gaps[1, 2] <= 0.6 * gaps[1, 1], gaps          # O(h): halves per refinement
+    assert gaps[1, 2] <= 0.04, gaps
 
 
 @pytest.mark.parametrize("p,prec,outer", [(1, 64, 0), (1, 32, 0), (2, 64, 0), (1, 64, 1)])

@@ -49,6 +49,46 @@ __global__ void k_bulk(const char *src, size_t per_cta, int bytes, int inflight,
   if (buf[0] == 123 && buf[1] == 45) sink[0] = 1;
 }
 
+// the ring kernels' pattern: CTA b streams "rows" of `bytes` bytes spaced
+// `stride` bytes apart (one strip of consecutive grid rows), neighbouring CTAs
+// on neighbouring strips (offset 2/3 of a row tile: strips overlap by halos)
+__global__ void k_bulk_rows(const char *src, size_t nrows, size_t stride, int bytes, int inflight,
+                            unsigned long long *sink) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sm);
+  unsigned char *buf = sm + 1024;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < inflight; i++)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar[i])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const char *base = src + (size_t)blockIdx.x * (bytes / 3 * 2 / 16 * 16);
+  for (size_t k = 0; k < nrows; k++) {
+    const int s = (int)(k % inflight);
+    if (k >= (size_t)inflight) {
+      const uint32_t par = (uint32_t)(((k / inflight) - 1) & 1);
+      uint32_t ok = 0;
+      while (!ok)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(ok) : "r"(su32(&bar[s])), "r"(par) : "memory");
+    }
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&bar[s])), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     su32(buf + (size_t)s * bytes)), "l"(base + k * stride), "r"(bytes), "r"(su32(&bar[s])) : "memory");
+  }
+  for (size_t k = nrows > (size_t)inflight ? nrows - inflight : 0; k < nrows; k++) {
+    const int s = (int)(k % inflight);
+    const uint32_t par = (uint32_t)((k / inflight) & 1);
+    uint32_t ok = 0;
+    while (!ok)
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(ok) : "r"(su32(&bar[s])), "r"(par) : "memory");
+  }
+  if (buf[0] == 123 && buf[1] == 45) sink[0] = 1;
+}
+
 __global__ void k_ldg(const int4 *src, size_t per_cta16, unsigned long long *sink) {
   const int4 *base = src + (size_t)blockIdx.x * per_cta16;
   int acc = 0;
@@ -72,6 +112,7 @@ int main() {
   CK(cudaMalloc(&sink, 64));
   CK(cudaMemset(src, 1, per_cta * nsm));
   CK(cudaFuncSetAttribute(k_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+  CK(cudaFuncSetAttribute(k_bulk_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
@@ -95,8 +136,48 @@ int main() {
              bytes * f / (gbs / nsm * 1e3));
       first = false;
     }
+  printf("\n], \"rows\": [\n");
+  first = true;
+  for (int bytes : {12288, 14336, 21504})
+    for (int f : {2, 4, 6, 8, 12}) {
+      if ((size_t)bytes * f > 200 * 1024) continue;
+      const size_t stride = 2516992;                  // one grid row of a c4 group (~820 pixels x 3 KB)
+      const size_t nrows = (per_cta * nsm - (size_t)nsm * bytes) / stride;
+      k_bulk_rows<<<nsm, 32, 1024 + bytes * f>>>(src, nrows, stride, bytes, f, sink);
+      CK(cudaEventRecord(e0));
+      k_bulk_rows<<<nsm, 32, 1024 + bytes * f>>>(src, nrows, stride, bytes, f, sink);
+      CK(cudaEventRecord(e1));
+      CK(cudaEventSynchronize(e1));
+      float ms;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      const double gbs = (double)nrows * bytes * nsm / (ms * 1e-3) / 1e9;
+      printf("%s  {\"bytes\": %d, \"inflight\": %d, \"gbs\": %.0f, \"per_sm_gbs\": %.1f, \"us_per_row\": %.3f, "
+             "\"latency_us\": %.2f}", first ? "" : ",\n", bytes, f, gbs, gbs / nsm, ms * 1e3 / nrows,
+             ms * 1e3 / nrows * f);
+      first = false;
+    }
   k_ldg<<<nsm, 256>>>((const int4 *)src, per_cta / 16, sink);
   CK(cudaEventRecord(e0));
+  printf("\n], \"rows\": [\n");
+  first = true;
+  for (int bytes : {12288, 14336, 21504})
+    for (int f : {2, 4, 6, 8, 12}) {
+      if ((size_t)bytes * f > 200 * 1024) continue;
+      const size_t stride = 2516992;                  // one grid row of a c4 group (~820 pixels x 3 KB)
+      const size_t nrows = (per_cta * nsm - (size_t)nsm * bytes) / stride;
+      k_bulk_rows<<<nsm, 32, 1024 + bytes * f>>>(src, nrows, stride, bytes, f, sink);
+      CK(cudaEventRecord(e0));
+      k_bulk_rows<<<nsm, 32, 1024 + bytes * f>>>(src, nrows, stride, bytes, f, sink);
+      CK(cudaEventRecord(e1));
+      CK(cudaEventSynchronize(e1));
+      float ms;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      const double gbs = (double)nrows * bytes * nsm / (ms * 1e-3) / 1e9;
+      printf("%s  {\"bytes\": %d, \"inflight\": %d, \"gbs\": %.0f, \"per_sm_gbs\": %.1f, \"us_per_row\": %.3f, "
+             "\"latency_us\": %.2f}", first ? "" : ",\n", bytes, f, gbs, gbs / nsm, ms * 1e3 / nrows,
+             ms * 1e3 / nrows * f);
+      first = false;
+    }
   k_ldg<<<nsm, 256>>>((const int4 *)src, per_cta / 16, sink);
   CK(cudaEventRecord(e1));
   CK(cudaEventSynchronize(e1));
