@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_pix(const double *z, int iters, 
     const int code = r < 45 ? 15 : r < 77 ? (15 & ~(1 << ((h >> 8) & 3))) : r < 96 ? ((h >> 10) & 1 ? 5 : 10) : 1;
     const int p = (h >> 12) % (NT - 8) + 2;
     auto ta = [&](int q) { return base + (uint32_t)q * PXB + lane_b; };
-    const double *zs = use_z ? z + ((size_t)((h >> 4) % 4096) * 6 * 64) + lane * NV : nullptr;
+    const double *zs = z + ((size_t)((h >> 4) % 4096) * 6 * 64) + lane * NV;
     pair_pixel<double, NV, P>(ta(p), ta(p + 1), ta(p - 1), ta((p + 17) % NT), ta((p + 41) % NT), code, zs, nullptr,
                               ta((p + 29) % NT), 0.75, 0.01, nullptr);
   }
@@ -68,11 +68,12 @@ int main() {
   CK(cudaMalloc(&z, (size_t)4096 * 6 * 64 * 8));
   CK(cudaMemset(z, 0, (size_t)4096 * 6 * 64 * 8));
   CK(cudaMalloc(&sink, 64));
-  for (int uz = 0; uz < 2; uz++) {
-    run<4>(z, sink, nsm, uz);
+  for (int uz = 1; uz < 2; uz++) {
     run<8>(z, sink, nsm, uz);
-    run<11>(z, sink, nsm, uz);
     run<12>(z, sink, nsm, uz);
+    run<14>(z, sink, nsm, uz);
+    run<16>(z, sink, nsm, uz);
+    run<20>(z, sink, nsm, uz);
   }
   return 0;
 }
