@@ -165,19 +165,19 @@ def cpu_model():
 
 
 def cpu_baseline(mask, sources, degree):
-    """O1 as it stands (test infrastructure) on the host: one source x one step
-    on one core, and nproc sources x one step on all cores (one OpenMP thread
-    per source); ~10-25 s on the c4 substrate."""
+    """O1 as it stands (test infrastructure) on the host: one source x two
+    steps on one core, and nproc sources x two steps on all cores (one OpenMP
+    thread per source); ~12 s on the c4 substrate."""
     th = oracle_threads()
     d = (degree + 1) * (degree + 2) // 2
     per = 2 * NX * NY * d                                   # element-dofs per source-step
-    t1 = oracle_sample(mask, sources[:1], degree, 1, 1)
-    ta = oracle_sample(mask, sources[:th], degree, th, 1)
-    one, allc = per / t1, th * per / ta
+    t1 = oracle_sample(mask, sources[:1], degree, 1, 2)
+    ta = oracle_sample(mask, sources[:th], degree, th, 2)
+    one, allc = 2 * per / t1, 2 * th * per / ta
     return {"value": allc, "unit": UNIT, "cores": th, "kind": "oracle",
             "one_core": one, "all_cores": allc, "nproc": os.cpu_count(), "cpu_model": cpu_model(),
-            "sample": f"same {NX}x{NY} c4 substrate, O1 fp64: 1 source x 1 SSP-RK3 step on 1 core ({t1:.1f} s) and "
-                      f"{th} sources x 1 step on {th} threads ({ta:.1f} s)"}
+            "sample": f"same {NX}x{NY} c4 substrate, O1 fp64: 1 source x 2 SSP-RK3 steps on 1 core ({t1:.1f} s) and "
+                      f"{th} sources x 2 steps on {th} threads ({ta:.1f} s)"}
 
 
 def run_reference(args):
@@ -213,6 +213,48 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- GPU arm
+def measure_k3d(args, dg, mask, batch, dt, nsteps, per_step, dofs, dist, stream, rank, world, local, nccl_id, peak):
+    """K3d (temporal_steps = 5: stage 1 on K2, stages 2 + 3 fused; bitwise equal
+    to K2) on the bench workload: 1 warm-up + k3d_steps timed steps."""
+    import torch
+    s = dg.Solver(mask, 1.0, 1.0, args.degree, precision=args.precision, rank=rank, nranks=world, nccl_id=nccl_id,
+                  stream=stream.cuda_stream, device=local, max_chunk=SRC_PER_GPU, temporal_steps=5)
+    try:
+        s.solve(batch(0), dt, nsteps)
+        S0, _ = s.covariance()
+        torch.cuda.synchronize()
+        dg.dgdiff_reset_stats(s.handle)
+        dg.dgdiff_set_timing(s.handle, 1)
+        if dist:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for k in range(args.k3d_steps):
+            s.solve(batch(args.warmup + k), dt, nsteps)
+            s.covariance()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        if dist:
+            t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = t.item()
+        st = s.stats()
+        pl_b = st["dom_bytes"] / max(1, st["dom_launches"])
+        pl_ms = st["dom_ms"] / max(1, st["dom_launches"])
+        ach = pl_b / (pl_ms * 1e-3) / 1e9 if pl_ms > 0 else None
+        return {"value": per_step * args.k3d_steps * dofs * nsteps / (ms * 1e-3), "unit": UNIT,
+                "ms_per_step": ms / args.k3d_steps, "steps": args.k3d_steps,
+                "sigma_first_batch": [S0[0, 0], S0[0, 1], S0[1, 1]],
+                "pair_kernel": {"achieved_gbs": ach, "frac_of_hbm": ach / peak if ach else None,
+                                "avg_launch_ms": pl_ms, "algorithmic_bytes_per_launch": pl_b,
+                                "share_of_step": st["dom_ms"] / ms if ms > 0 else None},
+                "note": "stage 1 on K2 + k_stage_pair (SSP-RK3 stages 2-3 fused, U2 in shared memory); "
+                        "5 state passes per step instead of 8; bitwise equal to K2"}
+    finally:
+        s.close()
+
+
 def run_ours(args):
     import torch
     world, rank, local = dist_env()
@@ -328,11 +370,16 @@ def run_ours(args):
         "library": {"env_overrides": st["env_overrides"], "tuning_build": st["tuning_build"],
                     "temporal_steps": args.temporal_steps},
     }
+    solver.close()
+    # the temporal-blocked path (K3d) on the same workload, beside the default
+    # K2 line: a short extra measurement (device time, same step definition)
+    if args.temporal_steps == 0 and args.degree == 1 and not args.windows and args.k3d_steps > 0:
+        line["k3d"] = measure_k3d(args, dg, mask, batch, dt, nsteps, per_step, dofs, dist, stream, rank, world,
+                                  local, nccl_id, peak)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(mask, all_src, args.degree)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    solver.close()
     if dist:
         dist.destroy_process_group()
     return 0
@@ -347,6 +394,8 @@ def main():
     ap.add_argument("--precision", type=int, default=64, choices=[64, 32])
     ap.add_argument("--degree", type=int, default=1, choices=[1, 2])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--k3d-steps", type=int, default=3,
+                    help="extra K3d steps timed beside the default K2 line (0 = skip)")
     ap.add_argument("--temporal-steps", type=int, default=DEFAULT_TS, choices=[0, 5],
                     help="0: K2, one launch per SSP-RK3 stage; 5: K3d, stages 2+3 fused (bitwise equal)")
     ap.add_argument("--windows", type=int, default=0, choices=[0, 1, 2],
