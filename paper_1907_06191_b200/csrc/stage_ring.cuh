@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
     k_stage_ring(const T *__restrict__ Uin, const T *U0, T *Uout, const int4 *__restrict__ nbr,
                  const int4 *__restrict__ rowtab, int nact, int ny, int nstrips, int ngroups, int band_rows,
                  int nitems, T alpha, T cs, int diag, int max_ahead, int n1_use, int n2_use,
-                 const T *__restrict__ Aabs, const int4 *__restrict__ gbox, int wr) {
+                 const T *__restrict__ Aabs, const int4 *__restrict__ gbox, int wr, int serial) {
   using Gm = RingGeom<T, NV, P, HAS_ALPHA>;
   constexpr int G = Gm::G, D2 = Gm::D2, PXB = Gm::PXB, Q = RING_Q, NC = Gm::NC;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -189,6 +189,56 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
       __syncwarp();
       const T *Ug = Uin + g * gstride;
       const T *U0g = U0 + g * gstride;
+      if (serial) {
+        // one lane issues the rows one at a time (see k_stage_pair: the batch
+        // issue re-runs its scan for every released row once the ring is full)
+        if (lane == 0) {
+          for (int r = lo; r <= hi; r++) {
+            const int4 t = rt[r - lo];
+            const bool comp = r >= jb0 && r < jb1;
+            const uint32_t n1 = (uint32_t)(t.w - t.x), n2 = comp ? (uint32_t)(t.z - t.y) : 0u;
+            for (;;) {
+              const uint32_t s1 = rel ? rv[(rel - 1) % Q] : 0u, s2 = rel ? rv[Q + (rel - 1) % Q] : 0u;
+              if ((L - rel < (uint32_t)max_ahead && v1 + n1 - s1 <= (uint32_t)n1_use && v2 + n2 - s2 <= (uint32_t)n2_use) ||
+                  rel == L)
+                break;
+              mbar_wait(&empty[rel % Q], (rel / Q) & 1);
+              rel++;
+            }
+            const uint32_t q = L % Q, p1 = v1 % Gm::N1, p2 = v2 % Gm::N2;
+            RowMeta m;
+            m.p1 = (int)p1; m.h0 = t.x; m.c0 = t.y; m.c1 = comp ? t.z : t.y; m.p2 = (int)p2;
+            m.pad0 = m.pad1 = m.pad2 = 0;
+            meta[q] = m;
+            v1 += n1;
+            v2 += n2;
+            rv[q] = v1;
+            rv[Q + q] = v2;
+            const uint32_t bytes = n1 * PXB + (Gm::R2U ? n2 * PXB : 0u) + n2 * 16u * Gm::NBW;
+            mbar_expect_tx(&full[q], bytes);
+            if (n1) {
+              const uint32_t a1 = min(n1, (uint32_t)Gm::N1 - p1);
+              const T *src = Ug + (size_t)t.x * D2 * G;
+              bulk_g2s(ring1 + (size_t)p1 * PXB, src, a1 * PXB, &full[q]);
+              if (n1 > a1) bulk_g2s(ring1, src + (size_t)a1 * D2 * G, (n1 - a1) * PXB, &full[q]);
+            }
+            if (n2) {
+              const uint32_t a2 = min(n2, (uint32_t)Gm::N2 - p2);
+              if (Gm::R2U) {
+                const T *src = U0g + (size_t)t.y * D2 * G;
+                bulk_g2s(ring2 + (size_t)p2 * PXB, src, a2 * PXB, &full[q]);
+                if (n2 > a2) bulk_g2s(ring2, src + (size_t)a2 * D2 * G, (n2 - a2) * PXB, &full[q]);
+              }
+              bulk_g2s(nbr_ring + (size_t)p2 * Gm::NBW, nbr + (size_t)t.y * Gm::NBW, a2 * 16u * Gm::NBW, &full[q]);
+              if (n2 > a2)
+                bulk_g2s(nbr_ring, nbr + ((size_t)t.y + a2) * Gm::NBW, (n2 - a2) * 16u * Gm::NBW, &full[q]);
+            }
+            L++;
+          }
+        }
+        __syncwarp();
+        continue;
+      }
       for (int r0 = lo; r0 <= hi;) {
         const int r = r0 + lane;
         const bool valid = r <= hi;
@@ -487,6 +537,20 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
   }
 }
 
+// producer mode: 1 = rows issued one at a time by one lane, 0 = warp-wide
+// batches.  Measured on c5 (64 sources, ms per stage, round 2): Q2 1.42 -> 1.32
+// with the serial issue, Q1 0.835 -> 0.829, P2 1.18 -> 1.22, P1 / P3 / c4 and
+// windows unchanged: serial for the quadrilaterals (DGDIFF_RING_SERIAL
+// overrides in tuning builds)
+template <int P>
+inline int ring_serial_producer() {
+  static const int v = [] {
+    const char *e = tune_env("DGDIFF_RING_SERIAL");
+    return e ? atoi(e) : (is_quad<P>() ? 1 : 0);
+  }();
+  return v;
+}
+
 // rows in flight per CTA (issued, not yet released): sparse rows stream best
 // with ~8 rows of lookahead, dense rows are limited by ring bytes first
 inline int alpha_max_ahead(const dgl::StageArgs &a, bool alpha) {
@@ -529,7 +593,8 @@ cudaError_t launch_ring(const dgl::StageArgs &a) {
       // (never below the progress minimum: ROWS_MIN full halo'd rows)
       Gm::R2U ? Gm::N1
               : std::max(Gm::ROWS_MIN * (Gm::W + 2 * Gm::HALO), std::min(Gm::N1, a.n1_use_na > 0 ? a.n1_use_na : Gm::N1)),
-      std::max(Gm::ROWS_MIN * Gm::W, std::min(Gm::N2, a.n2_use > 0 ? a.n2_use : Gm::N2)), (const T *)a.Aabs, a.gbox, a.wr);
+      std::max(Gm::ROWS_MIN * Gm::W, std::min(Gm::N2, a.n2_use > 0 ? a.n2_use : Gm::N2)), (const T *)a.Aabs, a.gbox, a.wr,
+      ring_serial_producer<P>());
   return cudaGetLastError();
 }
 
