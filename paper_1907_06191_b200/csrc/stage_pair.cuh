@@ -368,6 +368,7 @@ __global__ void __launch_bounds__(PairGeom<T, NV, P, NB_, NC_>::THREADS, 1)
           // ring-3 room for all of row j: C must have released everything
           // older than row j-2 (lazy allocation; see the header)
           const uint32_t need = mc.v3 + (uint32_t)(mc.c1 - mc.c0);
+          const long long t0 = clock64();
           for (;;) {
             uint32_t mn = ld_acquire_cta(&relv[0]);
 #pragma unroll
@@ -377,6 +378,7 @@ __global__ void __launch_bounds__(PairGeom<T, NV, P, NB_, NC_>::THREADS, 1)
             }
             if ((int)(need - mn) <= N3) break;
             __nanosleep(32);
+            if (clock64() - t0 > (1LL << 34)) __trap();   // watchdog, as mbar_wait
           }
           space_ok = true;
         }
