@@ -9,6 +9,7 @@
 // Block ids: 0 = V, 1..4 = F_E, F_W, F_N, F_S, 5..8 = N_E, N_W, N_N, N_S,
 // 9 + code = the full self block A[code][self] of that open-face code (used
 // by the kernels through a warp-uniform switch: 116 MACs per P1 pixel).
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -16,6 +17,73 @@
 #include <vector>
 
 #include "operator.h"
+
+// P3 column form for the ring kernel (round 2): the same V, F_f, N_f values as
+// TAB_P3 laid out column by column, so the kernel applies each block as a
+// short runtime loop over its non-zero columns (one broadcast shared-memory
+// load per two coefficients, all rows of a column at once) instead of ~100 KB
+// of straight-line code that overflows the instruction cache.  Layout:
+//   V            [D2 cols][D2 rows]
+//   per face f:  F_f [NCF][RF rows]  over columns P3COL_CF[f][] and the RF
+//                contiguous rows from P3COL_R0F[f] (F_f only touches the
+//                triangle that owns face f: checked here),
+//                N_f [NCN][D2 rows]  over columns P3COL_CN[f][]
+// Lists shorter than NCF / NCN are padded with column 0 and zero coefficients.
+static int emit_p3_columns(FILE *f, const std::vector<double> &blk, int D2) {
+  auto B = [&](int b, int r, int c) { return blk[((size_t)b * D2 + r) * D2 + c]; };
+  const int RF = D2 / 2;
+  std::vector<int> cf[4], cn[4];
+  int r0f[4], ncf = 0, ncn = 0;
+  for (int fb = 0; fb < 4; fb++) {
+    int rlo = D2, rhi = -1;
+    for (int c = 0; c < D2; c++) {
+      bool nzf = false, nzn = false;
+      for (int r = 0; r < D2; r++) {
+        if (B(1 + fb, r, c) != 0.0) { nzf = true; rlo = std::min(rlo, r); rhi = std::max(rhi, r); }
+        if (B(5 + fb, r, c) != 0.0) nzn = true;
+      }
+      if (nzf) cf[fb].push_back(c);
+      if (nzn) cn[fb].push_back(c);
+    }
+    r0f[fb] = rlo < RF ? 0 : RF;
+    if (rhi >= r0f[fb] + RF || rlo < r0f[fb]) {
+      fprintf(stderr, "p3 F_%d rows [%d, %d] not within one triangle\n", fb, rlo, rhi);
+      return 1;
+    }
+    ncf = std::max(ncf, (int)cf[fb].size());
+    ncn = std::max(ncn, (int)cn[fb].size());
+  }
+  if (ncf % 2) ncf++;   // the kernel's column loop is unrolled by two
+  if (ncn % 2) ncn++;
+  std::vector<double> col;
+  for (int c = 0; c < D2; c++)
+    for (int r = 0; r < D2; r++) col.push_back(B(0, r, c));
+  for (int fb = 0; fb < 4; fb++) {
+    for (int k = 0; k < ncf; k++)
+      for (int r = 0; r < RF; r++) col.push_back(k < (int)cf[fb].size() ? B(1 + fb, r0f[fb] + r, cf[fb][k]) : 0.0);
+    for (int k = 0; k < ncn; k++)
+      for (int r = 0; r < D2; r++) col.push_back(k < (int)cn[fb].size() ? B(5 + fb, r, cn[fb][k]) : 0.0);
+  }
+  fprintf(f, "// P3 column form (V, then per face F_f over NCF columns x %d rows and N_f over NCN columns x %d rows)\n",
+          RF, D2);
+  fprintf(f, "constexpr int P3COL_NCF = %d, P3COL_NCN = %d, P3COL_RF = %d, P3COL_N = %zu;\n", ncf, ncn, RF, col.size());
+  fprintf(f, "constexpr int P3COL_R0F[4] = {%d, %d, %d, %d};\n", r0f[0], r0f[1], r0f[2], r0f[3]);
+  for (int pass = 0; pass < 2; pass++) {
+    fprintf(f, "__device__ const unsigned char P3COL_%s[4][%d] = {", pass ? "CN" : "CF", pass ? ncn : ncf);
+    for (int fb = 0; fb < 4; fb++) {
+      const std::vector<int> &v = pass ? cn[fb] : cf[fb];
+      const int n = pass ? ncn : ncf;
+      fprintf(f, "{");
+      for (int k = 0; k < n; k++) fprintf(f, "%d%s", k < (int)v.size() ? v[k] : 0, k + 1 < n ? ", " : "");
+      fprintf(f, "}%s", fb < 3 ? ", " : "");
+    }
+    fprintf(f, "};\n");
+  }
+  fprintf(f, "#define DGK_P3COL_DATA \\\n");
+  for (size_t i = 0; i < col.size(); i++) fprintf(f, "%a,%s", col[i], (i % 8 == 7) ? " \\\n" : " ");
+  fprintf(f, "\n__device__ const double P3COL_D[%zu] = {DGK_P3COL_DATA};\n\n", col.size());
+  return 0;
+}
 
 static int emit(FILE *f, int p) {
   dgop::Table T = dgop::build(p);
@@ -66,7 +134,7 @@ static int emit(FILE *f, int p) {
                "  return TAB_P3_D[(b * %d + r) * %d + c];\n#else\n  return TAB_P3_H[(b * %d + r) * %d + c];\n#endif\n}\n",
             D2, D2, D2, D2);
     fprintf(f, "// nnz(P3) = %d\n\n", nnz);
-    return 0;
+    return emit_p3_columns(f, blk, D2);
   }
   fprintf(f, "__host__ __device__ constexpr double tab_p%d(int b, int r, int c) {\n  switch ((b * %d + r) * %d + c) {\n", p, D2, D2);
   int nnz = 0;

@@ -32,6 +32,7 @@
 #pragma once
 #include <algorithm>
 #include <atomic>
+#include <type_traits>
 #include <cstdlib>
 #include "kernels.cuh"
 #include "stage_imm.cuh"
@@ -81,6 +82,27 @@ template <> struct RingCfg<101, 8, RING_U0_DIRECT> { static constexpr int W = 16
 template <> struct RingCfg<102, 8, RING_PLAIN> { static constexpr int W = 8, NC = 8; };
 template <> struct RingCfg<102, 8, RING_U0_STAGED> { static constexpr int W = 8, NC = 8; };
 template <> struct RingCfg<102, 8, RING_U0_DIRECT> { static constexpr int W = 8, NC = 8; };
+// P3 operator application: column loops over a shared-memory table (round
+// 2, default) or the round-1 straight-line immediates (-DDGDIFF_P3_IMM)
+// (fp64 only: fp32 coefficients are 32-bit FFMA immediates, so the fp32
+// straight-line code is half the size and runs faster than the loops, c5:
+// 2.2 vs 3.8 ms per stage)
+#ifdef DGDIFF_P3_IMM
+template <typename T, int P> constexpr bool ring_p3_columns() { return false; }
+#else
+template <typename T, int P> constexpr bool ring_p3_columns() { return P == 3 && sizeof(T) == 8; }
+#endif
+
+#ifndef DGDIFF_P3COL_NC
+#define DGDIFF_P3COL_NC 11
+#endif
+#ifndef DGDIFF_P3COL_UNROLL   // column-loop unroll of the pair loop (c5: 1 / 2 / 4 swept)
+#define DGDIFF_P3COL_UNROLL 2
+#endif
+#ifndef DGDIFF_P3COL_NCA   // alpha stages (u0 loads): 8 warps, 255 registers
+#define DGDIFF_P3COL_NCA 7
+#endif
+
 template <int P> constexpr int ring_mode(bool alpha) {
   return alpha ? (ring_u0_direct<P>() ? RING_U0_DIRECT : RING_U0_STAGED) : RING_PLAIN;
 }
@@ -93,7 +115,11 @@ struct RingGeom {
   static constexpr int NBW = HALO;                               // int4 neighbour entries per pixel
   static constexpr bool R2U = ALPHA && !ring_u0_direct<P>();   // u0 tiles staged in ring 2
   static constexpr int W = RingCfg<P, NV * (int)sizeof(T), ring_mode<P>(ALPHA)>::W;
-  static constexpr int NC = RingCfg<P, NV * (int)sizeof(T), ring_mode<P>(ALPHA)>::NC;
+  // (P3 column form: pixel pairs hold two 20-dof accumulators; the register
+  // file is split over the 4 SM sub-partitions, so 12 warps per CTA leave 168
+  // registers per thread and 8 warps 255)
+  static constexpr int NC = ring_p3_columns<T, P>() ? (ALPHA ? DGDIFF_P3COL_NCA : DGDIFF_P3COL_NC)
+                                                   : RingCfg<P, NV * (int)sizeof(T), ring_mode<P>(ALPHA)>::NC;
   static constexpr int PXB = D2 * G * (int)sizeof(T);  // one pixel tile (one group)
   static constexpr int SMEM_MAX = 232448;
   static constexpr int EXTRA = 2 * RING_Q * 8 + RING_Q * 32 + (RING_MAXBAND + 4) * 16 + 2 * RING_Q * 4;
@@ -101,13 +127,21 @@ struct RingGeom {
   // only holds the 16-byte indices and ring 1 takes the rest
   static constexpr int N2 = R2U ? 4 * W : 16 * W;
   static constexpr int ROWS_MIN = 2 * HALO + 2;                 // rows held + 1 in flight
-  static constexpr int N1 = R2U ? ROWS_MIN * (W + 2 * HALO) : RING_N1_NOALPHA(W, PXB, SMEM_MAX - EXTRA - N2 * 16 * NBW);
+  // P3: the column-form operator (tables.inc P3COL_*) and its column lists
+  // live in shared memory (ring_p3_columns())
+  // (+ one zero lane vector: the x operand of a closed face in a pixel pair)
+  static constexpr int COLB = ring_p3_columns<T, P>()
+                                  ? ((P3COL_N * (int)sizeof(T) + 4 * (P3COL_NCF + P3COL_NCN) + 32 * NV * (int)sizeof(T) + 127) / 128) * 128
+                                  : 0;
+  static constexpr int UPX = COLB ? 2 : 1;   // pixels per consumer work unit (P3 column form: pairs)
+  static constexpr int N1 = R2U ? ROWS_MIN * (W + 2 * HALO) : RING_N1_NOALPHA(W, PXB, SMEM_MAX - EXTRA - COLB - N2 * 16 * NBW);
   static constexpr int OFF_R2 = N1 * PXB;
   static constexpr int OFF_NB = OFF_R2 + (R2U ? N2 * PXB : 0);
   static constexpr int OFF_BAR = OFF_NB + N2 * 16 * NBW;
   static constexpr int OFF_META = OFF_BAR + 2 * RING_Q * 8;
   static constexpr int OFF_RT = OFF_META + RING_Q * 32;
-  static constexpr int SMEM = OFF_RT + (RING_MAXBAND + 4) * 16 + 2 * RING_Q * 4;   // rows of a band + 2 halos
+  static constexpr int OFF_COL = OFF_RT + (RING_MAXBAND + 4) * 16 + 2 * RING_Q * 4;   // rows of a band + 2 halos
+  static constexpr int SMEM = OFF_COL + COLB;
   static constexpr int THREADS = (NC + 1) * 32;
   static_assert(SMEM <= SMEM_MAX, "ring does not fit in shared memory");
   static_assert(N1 >= ROWS_MIN * (W + 2 * HALO) && N2 >= ROWS_MIN * W, "rings too small for progress");
@@ -142,6 +176,61 @@ struct RowMeta {
 };
 
 
+// acc[R0 .. R0+R) += C x over the columns of a column-form block (P3): column
+// jj of C is the R contiguous coefficients cf[jj*R ..], applied to the dof
+// cols[jj] (identity when cols is null) of the pixel tile x (ring-1 slot,
+// this lane's sources).  A runtime loop: one warp-uniform (broadcast) shared-
+// memory load per two coefficients, so the code stays in the instruction
+// cache whatever the block; the loop is unrolled by two so the next column's
+// loads overlap this column's FMAs.
+template <typename T, int NV, int D2, int G, int R, int R0>
+__device__ __forceinline__ void colmv(T (&acc)[D2][NV], const T *__restrict__ cf, const unsigned char *__restrict__ cols,
+                                      int ncol, const T *__restrict__ x) {
+  typedef typename VT<T, 2>::type T2;
+#pragma unroll 2
+  for (int jj = 0; jj < ncol; jj++) {
+    const int c = cols ? (int)cols[jj] : jj;
+    T xv[NV];
+    lds<T, NV>(x + c * G, xv);
+    const T *cp = cf + jj * R;
+#pragma unroll
+    for (int r = 0; r < R; r += 2) {
+      const T2 cc = *reinterpret_cast<const T2 *>(cp + r);
+      fma_bc<T, NV>(cc.x, xv, acc[R0 + r]);
+      fma_bc<T, NV>(cc.y, xv, acc[R0 + r + 1]);
+    }
+  }
+}
+
+// The same for two pixels at once (a warp's pixel pair): each coefficient
+// load feeds both pixels' FMAs, which halves the shared-memory wavefronts per
+// FMA (one broadcast wavefront per coefficient is the limit of the one-pixel
+// loop: ncu, c5, L1 at 85 %).  A side whose face is closed reads the zero
+// vector (stride 0): it adds exact zeros.
+template <typename T, int NV, int D2, int R, int R0>
+__device__ __forceinline__ void colmv2(T (&accA)[D2][NV], T (&accB)[D2][NV], const T *__restrict__ cf,
+                                       const unsigned char *__restrict__ cols, int ncol, const T *__restrict__ xA,
+                                       int sA, const T *__restrict__ xB, int sB) {
+  typedef typename VT<T, 2>::type T2;
+  constexpr int kUnroll = DGDIFF_P3COL_UNROLL;
+#pragma unroll kUnroll
+  for (int jj = 0; jj < ncol; jj++) {
+    const int c = cols ? (int)cols[jj] : jj;
+    T va[NV], vb[NV];
+    lds<T, NV>(xA + c * sA, va);
+    lds<T, NV>(xB + c * sB, vb);
+    const T *cp = cf + jj * R;
+#pragma unroll
+    for (int r = 0; r < R; r += 2) {
+      const T2 cc = *reinterpret_cast<const T2 *>(cp + r);
+      fma_bc<T, NV>(cc.x, va, accA[R0 + r]);
+      fma_bc<T, NV>(cc.x, vb, accB[R0 + r]);
+      fma_bc<T, NV>(cc.y, va, accA[R0 + r + 1]);
+      fma_bc<T, NV>(cc.y, vb, accB[R0 + r + 1]);
+    }
+  }
+}
+
 template <typename T, int NV, int P, bool HAS_ALPHA>
 __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
     k_stage_ring(const T *__restrict__ Uin, const T *U0, T *Uout, const int4 *__restrict__ nbr,
@@ -165,6 +254,17 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
       mbar_init(&empty[q], NC);
     }
     fence_mbar_init();
+  }
+  T *colA = reinterpret_cast<T *>(smem + Gm::OFF_COL);
+  T *colZ = colA + (Gm::COLB ? P3COL_N : 0);   // 32 NV zeros (a closed face's x in a pair)
+  unsigned char *colI = smem + Gm::OFF_COL + (Gm::COLB ? (P3COL_N + 32 * NV) * (int)sizeof(T) : 0);
+  if constexpr (Gm::COLB > 0) {
+    // P3 column-form operator (state precision) and its column lists
+    for (int i = tid; i < P3COL_N; i += blockDim.x) colA[i] = (T)P3COL_D[i];
+    for (int i = tid; i < 32 * NV; i += blockDim.x) colZ[i] = (T)0;
+    for (int i = tid; i < 4 * (P3COL_NCF + P3COL_NCN); i += blockDim.x)
+      colI[i] = i < 4 * P3COL_NCF ? P3COL_CF[i / P3COL_NCF][i % P3COL_NCF]
+                                  : P3COL_CN[(i - 4 * P3COL_NCF) / P3COL_NCN][(i - 4 * P3COL_NCF) % P3COL_NCN];
   }
   __syncthreads();
   const size_t gstride = (size_t)nact * D2 * G;
@@ -340,9 +440,11 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
     int j = jb0, rel_next = lo, cum = 0;
     for (int r = jb0 - Gm::HALO; r <= jb0 + Gm::HALO; r++) wait_row(r);
     RowMeta mc = meta[seq(j) % Q];
+    constexpr int UPX = Gm::UPX;
     for (int f = w;; f += NC) {
-      while (f >= cum + (mc.c1 - mc.c0)) {      // advance the cursor to f's row
-        cum += mc.c1 - mc.c0;
+      // (work units: pixels, or pixel pairs within a row for the P3 column form)
+      while (f >= cum + (mc.c1 - mc.c0 + UPX - 1) / UPX) {      // advance the cursor to f's row
+        cum += (mc.c1 - mc.c0 + UPX - 1) / UPX;
         if (++j >= jb1) break;
         // this warp's remaining pixels lie in rows >= j: rows <= j-1-HALO have
         // had their last reader; release them before waiting for row j+HALO (a
@@ -358,7 +460,7 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
       }
       if (j >= jb1) break;
       if (diag == 1) continue;   // diagnostic: stream through the ring without computing
-      const int a = mc.c0 + (f - cum);
+      auto pixel = [&](const int a) {
       int sl2 = mc.p2 + (a - mc.c0);
       if (sl2 >= Gm::N2) sl2 -= Gm::N2;
       const int4 nb = nbr_ring[(size_t)sl2 * Gm::NBW];
@@ -370,8 +472,11 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
 #pragma unroll
         for (int k = 0; k < D2; k++) ldvc<T, NV>(U0l + ((size_t)a * D2 + k) * G, z[k]);
       }
+      // (column form: xs is read per column and again for the RK combination)
+      if constexpr (!Gm::COLB) {
 #pragma unroll
-      for (int k = 0; k < D2; k++) lds<T, NV>(ps + k * G, xs[k]);
+        for (int k = 0; k < D2; k++) lds<T, NV>(ps + k * G, xs[k]);
+      }
 #pragma unroll
       for (int k = 0; k < D2; k++)
 #pragma unroll
@@ -461,6 +566,33 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
           }
         }
         }   // interior / REFLECT quads
+      } else if (Gm::COLB && __builtin_expect(outer == 0, 1)) {
+        // P3 column form: V, then per open face F_f (the RF rows of the
+        // triangle owning face f) and N_f, each a loop over its columns
+        if constexpr (Gm::COLB > 0) {
+          constexpr int RF = P3COL_RF, NCF = P3COL_NCF, NCN = P3COL_NCN;
+          const T *cV = colA, *cF = colA + D2 * D2;
+          constexpr int FB = NCF * RF + NCN * D2;   // per-face block size
+          colmv<T, NV, D2, G, D2, 0>(acc, cV, nullptr, D2, ps);
+          if (nb.x >= 0) {
+            colmv<T, NV, D2, G, RF, P3COL_R0F[0]>(acc, cF + 0 * FB, colI + 0 * NCF, NCF, ps);
+            colmv<T, NV, D2, G, D2, 0>(acc, cF + 0 * FB + NCF * RF, colI + 4 * NCF + 0 * NCN, NCN, tile1(mc, nb.x));
+          }
+          if (nb.y >= 0) {
+            colmv<T, NV, D2, G, RF, P3COL_R0F[1]>(acc, cF + 1 * FB, colI + 1 * NCF, NCF, ps);
+            colmv<T, NV, D2, G, D2, 0>(acc, cF + 1 * FB + NCF * RF, colI + 4 * NCF + 1 * NCN, NCN, tile1(mc, nb.y));
+          }
+          if (nb.z >= 0) {
+            colmv<T, NV, D2, G, RF, P3COL_R0F[2]>(acc, cF + 2 * FB, colI + 2 * NCF, NCF, ps);
+            colmv<T, NV, D2, G, D2, 0>(acc, cF + 2 * FB + NCF * RF, colI + 4 * NCF + 2 * NCN, NCN,
+                                       tile1(meta[seq(j + 1) % Q], nb.z));
+          }
+          if (nb.w >= 0) {
+            colmv<T, NV, D2, G, RF, P3COL_R0F[3]>(acc, cF + 3 * FB, colI + 3 * NCF, NCF, ps);
+            colmv<T, NV, D2, G, D2, 0>(acc, cF + 3 * FB + NCF * RF, colI + 4 * NCF + 3 * NCN, NCN,
+                                       tile1(meta[seq(j - 1) % Q], nb.w));
+          }
+        }
       } else if (__builtin_expect(outer == 0, 1)) {
         // self block of this pixel's open-face code (compile-time immediates),
         // then the fixed neighbour blocks of the open faces
@@ -502,6 +634,10 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
         // boundary pixel with absorbing outer faces: blocks of (code, outer)
         // read from the K0 table in global memory (rare: grid-edge pixels)
         const T *Ab = Aabs + (size_t)((open_code(nb) * 16 + outer) * 5) * D2 * D2;
+        if constexpr (Gm::COLB > 0) {
+#pragma unroll
+          for (int k = 0; k < D2; k++) lds<T, NV>(ps + k * G, xs[k]);
+        }
         mv_gen<T, NV, D2>(acc, Ab, xs);
         const int nbv[4] = {nb.x, nb.y, nb.z, nb.w};
 #pragma unroll 1
@@ -518,6 +654,7 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
 #pragma unroll
       for (int k = 0; k < D2; k++) {
         T y[NV];
+        if constexpr (Gm::COLB > 0) lds<T, NV>(ps + k * G, xs[k]);
         if (HAS_ALPHA) {
           if constexpr (Gm::R2U) lds<T, NV>(pu + k * G, z[k]);
 #pragma unroll
@@ -527,6 +664,76 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
           for (int e = 0; e < NV; e++) y[e] = xs[k][e] + cs * acc[k][e];
         }
         stv<T, NV>(out + (size_t)k * G, y);
+      }
+      };   // pixel
+      if constexpr (UPX == 1) {
+        pixel(mc.c0 + (f - cum));
+      } else {
+        const int a = mc.c0 + 2 * (f - cum);
+        if (a + 1 < mc.c1) {
+          int sl2 = mc.p2 + (a - mc.c0), sl2b = sl2 + 1;
+          if (sl2 >= Gm::N2) sl2 -= Gm::N2;
+          if (sl2b >= Gm::N2) sl2b -= Gm::N2;
+          const int4 nA = nbr_ring[(size_t)sl2 * Gm::NBW], nB = nbr_ring[(size_t)sl2b * Gm::NBW];
+          const bool outer = nA.x == -2 || nA.y == -2 || nA.z == -2 || nA.w == -2 || nB.x == -2 || nB.y == -2 ||
+                             nB.z == -2 || nB.w == -2;
+          if (__builtin_expect(!outer, 1)) {
+            if constexpr (Gm::COLB > 0) {
+              // pixel pair (a, a + 1) of row j, P3 column form
+              constexpr int RF = P3COL_RF, NCF = P3COL_NCF, NCN = P3COL_NCN;
+              constexpr int FB = NCF * RF + NCN * D2;
+              const T *cV = colA, *cF = colA + D2 * D2;
+              const T *pA = tile1(mc, a), *pB = tile1(mc, a + 1);
+              T accA[D2][NV], accB[D2][NV];
+#pragma unroll
+              for (int k = 0; k < D2; k++)
+#pragma unroll
+                for (int e = 0; e < NV; e++) accA[k][e] = accB[k][e] = (T)0;
+              colmv2<T, NV, D2, D2, 0>(accA, accB, cV, nullptr, D2, pA, G, pB, G);
+              const T *zv = colZ + lane * NV;
+              // per face: F_f on the self tile and N_f on the neighbour tile of
+              // each pixel whose face is open (zeros for the other)
+              auto face = [&](auto fc, int ia, int ib, const RowMeta &mn) {
+                constexpr int fi = decltype(fc)::value;
+                if (ia < 0 && ib < 0) return;
+                colmv2<T, NV, D2, RF, P3COL_R0F[fi]>(accA, accB, cF + fi * FB, colI + fi * NCF, NCF, ia >= 0 ? pA : zv,
+                                                     ia >= 0 ? G : 0, ib >= 0 ? pB : zv, ib >= 0 ? G : 0);
+                colmv2<T, NV, D2, D2, 0>(accA, accB, cF + fi * FB + NCF * RF, colI + 4 * NCF + fi * NCN, NCN,
+                                         ia >= 0 ? tile1(mn, ia) : zv, ia >= 0 ? G : 0, ib >= 0 ? tile1(mn, ib) : zv,
+                                         ib >= 0 ? G : 0);
+              };
+              face(std::integral_constant<int, 0>(), nA.x, nB.x, mc);
+              face(std::integral_constant<int, 1>(), nA.y, nB.y, mc);
+              face(std::integral_constant<int, 2>(), nA.z, nB.z, meta[seq(j + 1) % Q]);
+              face(std::integral_constant<int, 3>(), nA.w, nB.w, meta[seq(j - 1) % Q]);
+              auto finish = [&](int ap, const T *pp, const T (&ac)[D2][NV]) {
+                T *out = Uog + (size_t)ap * D2 * G;
+#pragma unroll
+                for (int k = 0; k < D2; k++) {
+                  T xk[NV], y[NV];
+                  lds<T, NV>(pp + k * G, xk);
+                  if constexpr (HAS_ALPHA) {
+                    T zk[NV];
+                    ldvc<T, NV>(U0l + ((size_t)ap * D2 + k) * G, zk);
+#pragma unroll
+                    for (int e = 0; e < NV; e++) y[e] = xk[e] + alpha * (zk[e] - xk[e]) + cs * ac[k][e];
+                  } else {
+#pragma unroll
+                    for (int e = 0; e < NV; e++) y[e] = xk[e] + cs * ac[k][e];
+                  }
+                  stv<T, NV>(out + (size_t)k * G, y);
+                }
+              };
+              finish(a, pA, accA);
+              finish(a + 1, pB, accB);
+            }
+          } else {
+            pixel(a);
+            pixel(a + 1);
+          }
+        } else {
+          pixel(a);
+        }
       }
     }
     // release every row of the item not yet released by this warp
