@@ -987,3 +987,42 @@ def test_k3d_c1_and_random_masks_vs_oracle(dg, orc, cfg, prec):
             for k in (0, 44):
                 assert rel_l2(s.density(k), rd[k]) <= t["dens"], (p, k)
         assert mom_err(mom, rm) <= t["mom"], p
+
+
+_P3CROP = {}
+
+
+def _p3crop(orc, cfg):
+    """77 sources (the fp32 batch; fp64 takes the first 45) on the crop, O1 once."""
+    if not _P3CROP:
+        m = np.ascontiguousarray(cfg.mask("c5")[384:640, 384:640])
+        rng = np.random.default_rng(77)
+        free = np.argwhere(m[64:192, 64:192] == 0) + 64
+        pick = free[rng.choice(len(free), 77, replace=False)]
+        src = np.stack([pick[:, 1], pick[:, 0]], 1).astype(np.int32)
+        ref_m, ref_d = orc.solve(3, 1.0, 1.0, m, src, 1 / 256, 16, keep_density=True)
+        _P3CROP.update(m=m, src=src, ref_m=ref_m, ref_d=ref_d)
+    return _P3CROP
+
+
+@pytest.mark.parametrize("prec", [64, 32])
+def test_p3_gamma_crop_vs_oracle(dg, orc, cfg, prec):
+    """N4 P3 on a 256^2 crop of the c5 Gamma substrate (round 2: the fp64
+    kernel applies the column-form operator to pixel pairs): one chunk of two
+    source groups (the second ragged), 16 steps, every density, moment and
+    Sigma against O1.  Dense rows fill the ring to its minimum, pairs straddle
+    open and closed faces, single pixels end odd rows."""
+    d = _p3crop(orc, cfg)
+    G = 32 if prec == 64 else 64
+    n = G + 13
+    src, ref_m, ref_d = d["src"][:n], d["ref_m"][:n], d["ref_d"][:n]
+    with dg.Solver(d["m"], 1.0, 1.0, 3, precision=prec, keep_density=1, max_chunk=2 * G) as s:
+        s.solve(src, 1 / 256, 16)
+        S, mu = s.covariance()
+        mom = s.moments()
+        dens = [s.density(k) for k in range(n)]
+    t = TOL[prec]
+    assert max(rel_l2(dens[k], ref_d[k]) for k in range(n)) <= t["dens"]
+    assert mom_err(mom, ref_m) <= t["mom"]
+    R, _ = orc.sigma(ref_m)
+    assert sig_err(S, R) <= t["sig"]
