@@ -133,7 +133,10 @@ struct RingGeom {
   static constexpr int COLB = ring_p3_columns<T, P>()
                                   ? ((P3COL_N * (int)sizeof(T) + 4 * (P3COL_NCF + P3COL_NCN) + 32 * NV * (int)sizeof(T) + 127) / 128) * 128
                                   : 0;
-  static constexpr int UPX = COLB ? 2 : 1;   // pixels per consumer work unit (P3 column form: pairs)
+  // pixels per consumer work unit: P3 column form pairs (shared coefficient
+  // loads).  (Units of 2-4 consecutive quad pixels, one after the other, were
+  // measured for Q1/Q2 on c5 and were 0-7 % slower.)
+  static constexpr int UPX = COLB ? 2 : 1;
   static constexpr int N1 = R2U ? ROWS_MIN * (W + 2 * HALO) : RING_N1_NOALPHA(W, PXB, SMEM_MAX - EXTRA - COLB - N2 * 16 * NBW);
   static constexpr int OFF_R2 = N1 * PXB;
   static constexpr int OFF_NB = OFF_R2 + (R2U ? N2 * PXB : 0);
