@@ -413,6 +413,8 @@ struct dgdiff_s {
   int4 *d_rowtab = nullptr;  // [nstrips][ny] {h0, c0, c1, h1} for the ring kernel
   int4 *d_rowtab3 = nullptr; // [nstrips3][ny][2] u/U1/U2/output bounds for the fused step
   int4 *d_rowtab_na = nullptr; // ring row table of the stage without the alpha term
+  int4 *d_nbi[2] = {nullptr, nullptr};   // quads: strip-major neighbour tables [stage without / with alpha]
+  int *d_nbi_off[2] = {nullptr, nullptr};  // and their (strip, row) offsets [nstrips][ny + 1]
   int4 *d_rowtab_pair = nullptr; // K3d (fused stages 2+3): [nstrips_pair][ny][2]
   int nstrips_pair = 0;
   uint16_t *d_nbs_pair = nullptr;  // K3d strip-major neighbour table
@@ -592,6 +594,10 @@ static void release(dgdiff_s *H) {
   cudaFree(H->d_rowtab);
   cudaFree(H->d_rowtab3);
   cudaFree(H->d_rowtab_na);
+  for (int v = 0; v < 2; v++) {
+    cudaFree(H->d_nbi[v]);
+    cudaFree(H->d_nbi_off[v]);
+  }
   cudaFree(H->d_rowtab_pair);
   cudaFree(H->d_nbs_pair);
   cudaFree(H->d_pix);
@@ -764,6 +770,29 @@ static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
       // deeper TMA queues delay the row the consumers need next)
       double tiles = 0;
       for (const int4 &t : rtab) tiles += t.w - t.x;
+      if (H->quad) {
+        // item neighbour buffers (stage_ring.cuh, Gm::NBI): the neighbour
+        // entries of every strip's computed pixels, strip by strip, rows in
+        // order, so that an item (strip, band of rows) is one contiguous run
+        std::vector<int4> nbi;
+        std::vector<int> off((size_t)ns * (ny + 1));
+        nbi.reserve(nbr_q.size());
+        for (int s = 0; s < ns; s++)
+          for (int j = 0; j <= ny; j++) {
+            off[(size_t)s * (ny + 1) + j] = (int)(nbi.size() / 2);
+            if (j == ny) break;
+            const int4 t = rtab[(size_t)s * ny + j];
+            for (int a = t.y; a < t.z; a++) {
+              nbi.push_back(nbr_q[2 * (size_t)a]);
+              nbi.push_back(nbr_q[2 * (size_t)a + 1]);
+            }
+          }
+        if ((int64_t)nbi.size() != 2 * H->nact) return fail(DGDIFF_E_ARG, "strip-major neighbour table: pixel count");
+        CK(cudaMalloc(&H->d_nbi[va], sizeof(int4) * nbi.size()));
+        CK(cudaMemcpy(H->d_nbi[va], nbi.data(), sizeof(int4) * nbi.size(), cudaMemcpyHostToDevice));
+        CK(cudaMalloc(&H->d_nbi_off[va], sizeof(int) * off.size()));
+        CK(cudaMemcpy(H->d_nbi_off[va], off.data(), sizeof(int) * off.size(), cudaMemcpyHostToDevice));
+      }
       int4 *d = nullptr;
       CK(cudaMalloc(&d, sizeof(int4) * rtab.size()));
       CK(cudaMemcpy(d, rtab.data(), sizeof(int4) * rtab.size(), cudaMemcpyHostToDevice));
@@ -1117,6 +1146,10 @@ static dgdiff_status run_chunk(dgdiff_s *H, int64_t nvalid, int64_t chunk, doubl
   sa.n1_use = H->n1_use;
   sa.n1_use_na = H->n1_use > 0 ? H->n1_use : (int)(8.0 * H->mean_tile + 0.5);
   sa.rowtab_na = H->d_rowtab_na;
+  sa.nbi = H->d_nbi[1];
+  sa.nbi_off = H->d_nbi_off[1];
+  sa.nbi_na = H->d_nbi[0];
+  sa.nbi_off_na = H->d_nbi_off[0];
   sa.nstrips_na = H->nstrips_na;
   sa.n2_use = H->n2_use;
   sa.st = st;

@@ -34,6 +34,12 @@ struct StageArgs {
   unsigned wave_epoch = 0;
   // K3d: strip-major 16-bit neighbour table of the U2 pixels (see stage_pair.cuh)
   const uint16_t *nbs = nullptr;
+  // ring, quads: strip-major copies of the neighbour table (per strip, rows in
+  // order, each row's computed pixels) and their offsets [nstrips][ny + 1], for
+  // the alpha stages (nbi) and the stage without alpha (nbi_na; its strips may
+  // differ)
+  const int4 *nbi = nullptr, *nbi_na = nullptr;
+  const int *nbi_off = nullptr, *nbi_off_na = nullptr;
   cudaStream_t st = nullptr;
 };
 

@@ -122,11 +122,22 @@ struct RingGeom {
                                                    : RingCfg<P, NV * (int)sizeof(T), ring_mode<P>(ALPHA)>::NC;
   static constexpr int PXB = D2 * G * (int)sizeof(T);  // one pixel tile (one group)
   static constexpr int SMEM_MAX = 232448;
-  static constexpr int EXTRA = 2 * RING_Q * 8 + RING_Q * 32 + (RING_MAXBAND + 4) * 16 + 2 * RING_Q * 4;
+  static constexpr int EXTRA = 2 * RING_Q * 8 + 4 * 8 + RING_Q * 32 + (RING_MAXBAND + 4) * 16 + 2 * RING_Q * 4;
   // ring 2 holds staged u0 tiles (R2U) and neighbour indices; otherwise it
   // only holds the 16-byte indices and ring 1 takes the rest
   static constexpr int N2 = R2U ? 4 * W : 16 * W;
   static constexpr int ROWS_MIN = 2 * HALO + 2;                 // rows held + 1 in flight
+  // item neighbour buffer (quads, round 2): the neighbour indices of an
+  // item's computed pixels arrive in ONE bulk copy per item from a strip-major
+  // copy of the table (nbi), into one of two item buffers of NBI_CAP pixels,
+  // instead of one copy per row into ring 2: a row then costs one bulk copy
+  // (a 1-D bulk copy costs the SM's TMA ~0.3 us whatever its size, and the
+  // quad kernels were bound by that row pipeline: c5 Q2 streams its rows in
+  // 1.08 of 1.28 ms without computing).  Bands are capped at NBI_ROWS rows.
+  static constexpr bool NBI = is_quad<P>() && !R2U;
+  static constexpr int NBI_ROWS = 64;
+  static constexpr int NBI_CAP = NBI ? NBI_ROWS * W : 0;
+  static constexpr int NBR_BYTES = NBI ? 2 * NBI_CAP * 16 * NBW : N2 * 16 * NBW;
   // P3: the column-form operator (tables.inc P3COL_*) and its column lists
   // live in shared memory (ring_p3_columns())
   // (+ one zero lane vector: the x operand of a closed face in a pixel pair)
@@ -137,11 +148,12 @@ struct RingGeom {
   // loads).  (Units of 2-4 consecutive quad pixels, one after the other, were
   // measured for Q1/Q2 on c5 and were 0-7 % slower.)
   static constexpr int UPX = COLB ? 2 : 1;
-  static constexpr int N1 = R2U ? ROWS_MIN * (W + 2 * HALO) : RING_N1_NOALPHA(W, PXB, SMEM_MAX - EXTRA - COLB - N2 * 16 * NBW);
+  static_assert(!(NBI && UPX != 1), "item neighbour buffers index pixels by their unit");
+  static constexpr int N1 = R2U ? ROWS_MIN * (W + 2 * HALO) : RING_N1_NOALPHA(W, PXB, SMEM_MAX - EXTRA - COLB - NBR_BYTES);
   static constexpr int OFF_R2 = N1 * PXB;
   static constexpr int OFF_NB = OFF_R2 + (R2U ? N2 * PXB : 0);
-  static constexpr int OFF_BAR = OFF_NB + N2 * 16 * NBW;
-  static constexpr int OFF_META = OFF_BAR + 2 * RING_Q * 8;
+  static constexpr int OFF_BAR = OFF_NB + NBR_BYTES;
+  static constexpr int OFF_META = OFF_BAR + 2 * RING_Q * 8 + 4 * 8;   // + item full / empty barriers
   static constexpr int OFF_RT = OFF_META + RING_Q * 32;
   static constexpr int OFF_COL = OFF_RT + (RING_MAXBAND + 4) * 16 + 2 * RING_Q * 4;   // rows of a band + 2 halos
   static constexpr int SMEM = OFF_COL + COLB;
@@ -239,7 +251,8 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
     k_stage_ring(const T *__restrict__ Uin, const T *U0, T *Uout, const int4 *__restrict__ nbr,
                  const int4 *__restrict__ rowtab, int nact, int ny, int nstrips, int ngroups, int band_rows,
                  int nitems, T alpha, T cs, int diag, int max_ahead, int n1_use, int n2_use,
-                 const T *__restrict__ Aabs, const int4 *__restrict__ gbox, int wr, int serial) {
+                 const T *__restrict__ Aabs, const int4 *__restrict__ gbox, int wr, int serial,
+                 const int4 *__restrict__ nbi, const int *__restrict__ nbi_off) {
   using Gm = RingGeom<T, NV, P, HAS_ALPHA>;
   constexpr int G = Gm::G, D2 = Gm::D2, PXB = Gm::PXB, Q = RING_Q, NC = Gm::NC;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -248,6 +261,7 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
   int4 *nbr_ring = reinterpret_cast<int4 *>(smem + Gm::OFF_NB);
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + Gm::OFF_BAR);
   uint64_t *empty = full + Q;
+  uint64_t *ifull = full + 2 * Q, *iempty = ifull + 2;   // item neighbour buffers (Gm::NBI)
   RowMeta *meta = reinterpret_cast<RowMeta *>(smem + Gm::OFF_META);
   int4 *rt = reinterpret_cast<int4 *>(smem + Gm::OFF_RT);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -255,6 +269,10 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
     for (int q = 0; q < Q; q++) {
       mbar_init(&full[q], 1);
       mbar_init(&empty[q], NC);
+    }
+    for (int b = 0; b < 2; b++) {
+      mbar_init(&ifull[b], 1);
+      mbar_init(&iempty[b], NC);
     }
     fence_mbar_init();
   }
@@ -283,6 +301,7 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
     uint32_t L = 0;                 // row loads issued by this CTA
     uint32_t v1 = 0, v2 = 0;        // virtual slot counters of rings 1 and 2
     uint32_t rel = 0;               // rows whose release has been observed
+    uint32_t icount = 0;            // items issued (NBI buffers)
     for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
       int s, g, jb0, jb1;
       if (!ring_item<Gm::W>(item, nstrips, ngroups, band_rows, ny, gbox, wr, s, g, jb0, jb1)) continue;
@@ -292,14 +311,28 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
       __syncwarp();
       const T *Ug = Uin + g * gstride;
       const T *U0g = U0 + g * gstride;
-      if (serial) {
+      if constexpr (Gm::NBI) {
+        // the item's neighbour entries: one bulk copy into item buffer b once
+        // the consumers are done with the item that used it two items ago
+        if (lane == 0) {
+          const uint32_t b = icount & 1;
+          if (icount >= 2) mbar_wait(&iempty[b], ((icount - 2) >> 1) & 1);
+          const int o0 = __ldg(&nbi_off[(size_t)s * (ny + 1) + jb0]), o1 = __ldg(&nbi_off[(size_t)s * (ny + 1) + jb1]);
+          if (o1 - o0 > Gm::NBI_CAP) __trap();   // the launcher caps the bands
+          const uint32_t bytes = (uint32_t)(o1 - o0) * 16u * Gm::NBW;
+          mbar_expect_tx(&ifull[b], bytes);
+          if (bytes) bulk_g2s(nbr_ring + (size_t)b * Gm::NBI_CAP * Gm::NBW, nbi + (size_t)o0 * Gm::NBW, bytes, &ifull[b]);
+        }
+        icount++;
+      }
+      if (serial || Gm::NBI) {
         // one lane issues the rows one at a time (see k_stage_pair: the batch
         // issue re-runs its scan for every released row once the ring is full)
         if (lane == 0) {
           for (int r = lo; r <= hi; r++) {
             const int4 t = rt[r - lo];
             const bool comp = r >= jb0 && r < jb1;
-            const uint32_t n1 = (uint32_t)(t.w - t.x), n2 = comp ? (uint32_t)(t.z - t.y) : 0u;
+            const uint32_t n1 = (uint32_t)(t.w - t.x), n2 = comp && !Gm::NBI ? (uint32_t)(t.z - t.y) : 0u;
             for (;;) {
               const uint32_t s1 = rel ? rv[(rel - 1) % Q] : 0u, s2 = rel ? rv[Q + (rel - 1) % Q] : 0u;
               if ((L - rel < (uint32_t)max_ahead && v1 + n1 - s1 <= (uint32_t)n1_use && v2 + n2 - s2 <= (uint32_t)n2_use) ||
@@ -422,9 +455,14 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
   // the warps work on several rows at once.  A warp releases row r once its
   // cursor has passed row r + 1.
   uint32_t Lbase = 0;
+  uint32_t icount = 0;   // items consumed (NBI buffers)
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
     int s_, g, jb0, jb1;
     if (!ring_item<Gm::W>(item, nstrips, ngroups, band_rows, ny, gbox, wr, s_, g, jb0, jb1)) continue;
+    // (NBI: the item's neighbour entries, indexed by the pixel's position f in
+    // the band's computed pixels)
+    const int4 *nbb = nbr_ring + (size_t)(icount & 1) * Gm::NBI_CAP * Gm::NBW;
+    if constexpr (Gm::NBI) mbar_wait(&ifull[icount & 1], (icount >> 1) & 1);
     const int lo = max(0, jb0 - Gm::HALO), hi = min(ny - 1, jb1 - 1 + Gm::HALO);
     T *Uog = Uout + g * gstride + lane * NV;
     const T *U0l = U0 + g * gstride + lane * NV;
@@ -466,7 +504,8 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
       auto pixel = [&](const int a) {
       int sl2 = mc.p2 + (a - mc.c0);
       if (sl2 >= Gm::N2) sl2 -= Gm::N2;
-      const int4 nb = nbr_ring[(size_t)sl2 * Gm::NBW];
+      const int4 *nbp = Gm::NBI ? nbb + (size_t)f * Gm::NBW : nbr_ring + (size_t)sl2 * Gm::NBW;
+      const int4 nb = nbp[0];
       const T *ps = tile1(mc, a);
       T xs[D2][NV], acc[D2][NV], xn[D2][NV], z[D2][NV];
       if constexpr (HAS_ALPHA && !Gm::R2U) {
@@ -490,7 +529,7 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
         // N4 Q_p: self[code] + per open face the neighbour block (two variants:
         // opposite face open / closed) and the far block of the pixel two
         // steps on (when extracellular); the corners couple to nothing
-        const int4 nb2 = nbr_ring[(size_t)sl2 * Gm::NBW + 1];
+        const int4 nb2 = nbp[1];
         const int code = open_code(nb);
         const int far_out = (nb2.x == -2) | ((nb2.y == -2) << 1) | ((nb2.z == -2) << 2) | ((nb2.w == -2) << 3);
         if (__builtin_expect((outer | far_out) != 0, 0)) {
@@ -741,8 +780,11 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
     }
     // release every row of the item not yet released by this warp
     __syncwarp();
-    if (lane == 0)
+    if (lane == 0) {
       for (int r = rel_next; r <= hi; r++) mbar_arrive(&empty[seq(r) % Q]);
+      if constexpr (Gm::NBI) mbar_arrive(&iempty[icount & 1]);
+    }
+    icount++;
     Lbase += (uint32_t)(hi - lo + 1);
   }
 }
@@ -792,6 +834,10 @@ cudaError_t launch_ring(const dgl::StageArgs &a) {
   static const int env_band = tune_env("DGDIFF_K2_BAND") ? atoi(tune_env("DGDIFF_K2_BAND")) : 0;   // diagnostic
   if (env_band > 0) band_rows = std::min(band_rows, env_band);
   if (band_rows > RING_MAXBAND) band_rows = RING_MAXBAND;
+  if (Gm::NBI) {
+    if (!(ALPHA ? a.nbi : a.nbi_na)) return cudaErrorInvalidValue;
+    band_rows = std::min(band_rows, Gm::NBI_ROWS);   // the item buffer holds NBI_ROWS full rows
+  }
   nbands = (a.ny + band_rows - 1) / band_rows;
   const int nitems = per_band * nbands;
   const int grid = std::min(nitems, a.nsm);
@@ -804,7 +850,7 @@ cudaError_t launch_ring(const dgl::StageArgs &a) {
       Gm::R2U ? Gm::N1
               : std::max(Gm::ROWS_MIN * (Gm::W + 2 * Gm::HALO), std::min(Gm::N1, a.n1_use_na > 0 ? a.n1_use_na : Gm::N1)),
       std::max(Gm::ROWS_MIN * Gm::W, std::min(Gm::N2, a.n2_use > 0 ? a.n2_use : Gm::N2)), (const T *)a.Aabs, a.gbox, a.wr,
-      ring_serial_producer<P>());
+      ring_serial_producer<P>(), ALPHA ? a.nbi : a.nbi_na, ALPHA ? a.nbi_off : a.nbi_off_na);
   return cudaGetLastError();
 }
 
