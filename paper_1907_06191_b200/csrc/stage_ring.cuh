@@ -76,12 +76,25 @@ template <> struct RingCfg<3, 8, RING_U0_DIRECT> { static constexpr int W = 8, N
 // N4 quadrilaterals: degree codes 101 (Q1), 102 (Q2); their composite
 // operator is a 9-point cross, so strips carry a 2-column halo, a pixel of
 // row j reads rows j-2..j+2 and each pixel has 8 neighbour indices
-template <> struct RingCfg<101, 8, RING_PLAIN> { static constexpr int W = 16, NC = 8; };
+// (Q1 with item neighbour buffers, c5: 8 / 11 / 15 / 19 / 23 / 31 consumer
+// warps -> 0.76 / 0.63 / 0.57 / 0.57 / 0.59 / 0.65 ms stage 1)
+#ifndef DGDIFF_Q1_NC
+#define DGDIFF_Q1_NC 15
+#endif
+template <> struct RingCfg<101, 8, RING_PLAIN> { static constexpr int W = 16, NC = DGDIFF_Q1_NC; };
 template <> struct RingCfg<101, 8, RING_U0_STAGED> { static constexpr int W = 16, NC = 8; };
-template <> struct RingCfg<101, 8, RING_U0_DIRECT> { static constexpr int W = 16, NC = 8; };
-template <> struct RingCfg<102, 8, RING_PLAIN> { static constexpr int W = 8, NC = 8; };
+template <> struct RingCfg<101, 8, RING_U0_DIRECT> { static constexpr int W = 16, NC = DGDIFF_Q1_NC; };
+// (Q2 with item neighbour buffers, c5: 6 / 8 / 11 / 15 consumer warps ->
+// 1.34 / 1.22 / 1.11 / 1.11 ms stage 1)
+#ifndef DGDIFF_Q2_NC
+#define DGDIFF_Q2_NC 11
+#endif
+#ifndef DGDIFF_Q2_NCA
+#define DGDIFF_Q2_NCA 11
+#endif
+template <> struct RingCfg<102, 8, RING_PLAIN> { static constexpr int W = 8, NC = DGDIFF_Q2_NC; };
 template <> struct RingCfg<102, 8, RING_U0_STAGED> { static constexpr int W = 8, NC = 8; };
-template <> struct RingCfg<102, 8, RING_U0_DIRECT> { static constexpr int W = 8, NC = 8; };
+template <> struct RingCfg<102, 8, RING_U0_DIRECT> { static constexpr int W = 8, NC = DGDIFF_Q2_NCA; };
 // P3 operator application: column loops over a shared-memory table (round
 // 2, default) or the round-1 straight-line immediates (-DDGDIFF_P3_IMM)
 // (fp64 only: fp32 coefficients are 32-bit FFMA immediates, so the fp32
