@@ -1026,3 +1026,28 @@ def test_p3_gamma_crop_vs_oracle(dg, orc, cfg, prec):
     assert mom_err(mom, ref_m) <= t["mom"]
     R, _ = orc.sigma(ref_m)
     assert sig_err(S, R) <= t["sig"]
+
+
+def test_q2_gamma_crop_full_bands_vs_oracle(dg, orc, cfg):
+    """N4 Q2 on a 512 x 600 crop of the c5 Gamma substrate: 75 strips x 2
+    source groups put the ring kernel at its 64-row band cap, so the item
+    neighbour buffers (one bulk copy per item from the strip-major table)
+    run full; one chunk of 37 sources (the second group ragged), 8 steps,
+    every density, moment and Sigma against O1's quad path."""
+    m = np.ascontiguousarray(cfg.mask("c5")[256:768, 200:800])
+    rng = np.random.default_rng(45)
+    free = np.argwhere(m[176:336, 220:380] == 0) + (176, 220)
+    pick = free[rng.choice(len(free), 37, replace=False)]
+    src = np.stack([pick[:, 1], pick[:, 0]], 1).astype(np.int32)
+    dt, nst = 1 / 64, 8
+    ref_m, ref_d = orc.q_solve(2, 1.0, 1.0, m, src, dt, nst, keep_density=True)
+    with dg.Solver(m, 1.0, 1.0, 2, keep_density=1, max_chunk=64, element=1) as s:
+        s.solve(src, dt, nst)
+        S, mu = s.covariance()
+        mom = s.moments()
+        err = max(rel_l2(s.density(k), ref_d[k]) for k in range(37))
+    t = TOL[64]
+    assert err <= t["dens"]
+    assert mom_err(mom, ref_m) <= t["mom"]
+    R, _ = orc.sigma(ref_m)
+    assert sig_err(S, R) <= t["sig"]
