@@ -76,7 +76,10 @@ typedef struct {
                              quads, P3; 4 and 5 need kernel 0 */
   int32_t device;         /* CUDA device ordinal; -1 = current device */
   int32_t rank, nranks;   /* source sharding: rank takes the contiguous block
-                             [rank*n/nranks, (rank+1)*n/nranks) of every batch */
+                             [rank*n/nranks, (rank+1)*n/nranks) of every batch
+                             (with windows != 0: that block of the batch in
+                             Morton order, so every rank's sources stay
+                             spatially compact; every rank sorts the same list) */
   const void *nccl_id;    /* ncclUniqueId* (128 bytes): the handle joins an
                              NCCL communicator of nranks ranks (with nranks == 1
                              a one-rank communicator).  NULL with nranks > 1 =
@@ -105,9 +108,9 @@ typedef struct {
                              units) during dgdiff_solve_batch, for
                              dgdiff_mixture; 0 (default) = off */
   int32_t windows;        /* N1 active windows ("the outer
-                             boundary is not reached"): 1 = sort this rank's
-                             sources spatially (Morton order) into source
-                             groups and, at every RK stage, compute only the
+                             boundary is not reached"): 1 = sort the batch
+                             spatially (Morton order) before sharding, into
+                             source groups, and, at every RK stage, compute only the
                              rows / column strips inside each group's source
                              box grown by one pixel per stage so far.  Exact:
                              the 5-point operator spreads support by one pixel

@@ -469,7 +469,7 @@ struct dgdiff_s {
   int64_t gbox_cap = 0;
   int wband = 32;                                  // ring band rows under windows (env DGDIFF_WBAND; swept 12-256 on c4)
   std::vector<int4> h_gbox;
-  std::vector<int64_t> h_spos;                     // local index -> sorted position
+  std::vector<int64_t> h_spos;                     // N1: global source index -> position in this rank's chunk order (-1: other rank)
   std::vector<int> h_pre;                          // 2-D prefix counts of active pixels [(ny+1)][(nx+1)]
   int64_t last_chunk_pos0 = 0;                     // sorted position of the last chunk's first source
   // mixture grid (N2)
@@ -1447,8 +1447,14 @@ static dgdiff_status solve_impl(dgdiff_s *H, const int32_t *sources, const doubl
   CK(cudaMemcpyAsync(H->d_src, H->h_src_stage.data(), sizeof(int32_t) * 2 * n, cudaMemcpyHostToDevice, H->stream));
   H->st.h2d_bytes += sizeof(int32_t) * 2 * n;
   std::vector<int32_t> srt;   // N1: this rank's sources in Morton order
-  std::vector<int64_t> ord(std::max<int64_t>(nloc, 0));   // chunk order -> local index
-  for (int64_t k = 0; k < nloc; k++) ord[k] = k;
+  // chunk order -> global source index: the contiguous shard [b, e), or under
+  // N1 windows the shard [b, e) of the WHOLE batch in Morton order (every rank
+  // sorts the same list the same way), so that each rank's source groups are
+  // spatially compact whatever the number of ranks (sorting within a
+  // contiguous shard of a random source list spreads each rank's sources over
+  // the whole box: 8 logical ranks on c4 ran 1.6x the one-rank work)
+  std::vector<int64_t> ord(std::max<int64_t>(nloc, 0));
+  for (int64_t k = 0; k < nloc; k++) ord[k] = b + k;
   if (nloc > 0 && H->windows) {
     auto morton = [](uint32_t x, uint32_t y) {
       uint64_t k = 0;
@@ -1456,17 +1462,19 @@ static dgdiff_status solve_impl(dgdiff_s *H, const int32_t *sources, const doubl
         k |= (uint64_t)((x >> bit) & 1) << (2 * bit) | (uint64_t)((y >> bit) & 1) << (2 * bit + 1);
       return k;
     };
-    std::stable_sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) {
-      return morton(sources[2 * (b + x)], sources[2 * (b + x) + 1]) <
-             morton(sources[2 * (b + y)], sources[2 * (b + y) + 1]);
+    std::vector<int64_t> all(n);
+    for (int64_t k = 0; k < n; k++) all[k] = k;
+    std::stable_sort(all.begin(), all.end(), [&](int64_t x, int64_t y) {
+      return morton(sources[2 * x], sources[2 * x + 1]) < morton(sources[2 * y], sources[2 * y + 1]);
     });
+    for (int64_t k = 0; k < nloc; k++) ord[k] = all[b + k];
     srt.resize(2 * nloc);
     std::vector<int32_t> perm(nloc);
-    H->h_spos.assign(nloc, 0);
+    H->h_spos.assign(n, -1);
     for (int64_t k = 0; k < nloc; k++) {
-      srt[2 * k] = sources[2 * (b + ord[k])];
-      srt[2 * k + 1] = sources[2 * (b + ord[k]) + 1];
-      perm[k] = (int32_t)(b + ord[k]);
+      srt[2 * k] = sources[2 * ord[k]];
+      srt[2 * k + 1] = sources[2 * ord[k] + 1];
+      perm[k] = (int32_t)ord[k];
       H->h_spos[ord[k]] = k;
     }
     if (nloc > H->srcw_cap) {
@@ -1486,7 +1494,7 @@ static dgdiff_status solve_impl(dgdiff_s *H, const int32_t *sources, const doubl
   if (nloc > 0 && px) {
     std::vector<double> rows((size_t)nloc * PXS);
     for (int64_t k = 0; k < nloc; k++)
-      memcpy(&rows[(size_t)k * PXS], px + (size_t)(b + ord[k]) * PXS, sizeof(double) * PXS);
+      memcpy(&rows[(size_t)k * PXS], px + (size_t)ord[k] * PXS, sizeof(double) * PXS);
     if (nloc > H->px_cap) {
       cudaFree(H->d_px);
       H->d_px = nullptr;
@@ -1834,10 +1842,8 @@ extern "C" dgdiff_status dgdiff_get_density(dgdiff_t H, int64_t src, double *out
   if (!H->solved || !H->o.keep_density) return fail(DGDIFF_E_STATE, "needs keep_density and a solve");
   int64_t k = src - H->last_chunk_begin;
   if (H->windows) {
-    // N1: chunks hold the rank's sources in Morton order
-    int64_t b, e;
-    dgdiff_shard(H->last_n, H->o.rank, H->o.nranks, &b, &e);
-    k = (src >= b && src < e) ? H->h_spos[src - b] - H->last_chunk_pos0 : -1;
+    // N1: chunks hold the rank's share of the Morton-ordered batch
+    k = (src >= 0 && src < (int64_t)H->h_spos.size() && H->h_spos[src] >= 0) ? H->h_spos[src] - H->last_chunk_pos0 : -1;
   }
   if (k < 0 || k >= H->last_chunk_n)
     return fail(DGDIFF_E_STATE, "source %lld is not in this rank's last chunk", (long long)src);

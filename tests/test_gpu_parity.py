@@ -855,8 +855,9 @@ def test_logical_ranks_bitwise(dg, cfg, windows):
     [r n/R, (r+1) n/R) into a zero-padded [n][6] table; the host sums the R
     tables (what ncclAllReduce does: disjoint rows plus zeros, exact) and K5
     reduces it in source order, so moments and Sigma are BITWISE those of one
-    rank, for R = 2, 4, 8 -- with and without N1 windows (per-rank Morton
-    sort and the perm scatter of the rows)."""
+    rank, for R = 2, 4, 8 -- with and without N1 windows (the batch is
+    Morton-sorted before sharding, and the perm scatter puts each rank's rows
+    back in input order)."""
     m = cfg.mask("c3")
     src = cfg.sources("c3", 1000)
     nsteps = 24
@@ -866,17 +867,26 @@ def test_logical_ranks_bitwise(dg, cfg, windows):
         M1 = s.moments()
     for R in (2, 4, 8):
         tab = np.zeros_like(M1)
+        owner = np.full(len(src), -1)
         for r in range(R):
             with dg.Solver(m, 1.0, 1.0, 1, windows=windows, rank=r, nranks=R) as s:
                 s.solve(src, 1 / 32, nsteps)
                 Mr = s.moments()
                 b, e = dg.dgdiff_shard(len(src), r, R)
-                assert np.all(Mr[:b] == 0) and np.all(Mr[e:] == 0)
+                mine = np.flatnonzero(np.any(Mr != 0, axis=1))
+                if windows:
+                    # the shard [b, e) of the batch in Morton order: e - b rows,
+                    # disjoint from the other ranks'
+                    assert len(mine) == e - b and np.all(owner[mine] == -1)
+                else:
+                    assert np.all(Mr[:b] == 0) and np.all(Mr[e:] == 0)
+                owner[mine] = r
                 with pytest.raises(dg.DGDiffError):
                     s.covariance()                               # a logical rank holds only its shard
                 tab += Mr
                 if r == R - 1:
                     SR, muR = s.covariance_table(tab)
+        assert np.all(owner >= 0)
         assert np.array_equal(tab, M1), R
         assert np.array_equal(SR, S1) and np.array_equal(muR, mu1), R
 
