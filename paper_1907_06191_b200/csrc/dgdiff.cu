@@ -1462,11 +1462,13 @@ static dgdiff_status solve_impl(dgdiff_s *H, const int32_t *sources, const doubl
         k |= (uint64_t)((x >> bit) & 1) << (2 * bit) | (uint64_t)((y >> bit) & 1) << (2 * bit + 1);
       return k;
     };
+    // (keys once, then one sort of (key, index) pairs: the index breaks ties,
+    // i.e. a stable order)
+    std::vector<std::pair<uint64_t, int64_t>> key(n);
+    for (int64_t k = 0; k < n; k++) key[k] = {morton(sources[2 * k], sources[2 * k + 1]), k};
+    std::sort(key.begin(), key.end());
     std::vector<int64_t> all(n);
-    for (int64_t k = 0; k < n; k++) all[k] = k;
-    std::stable_sort(all.begin(), all.end(), [&](int64_t x, int64_t y) {
-      return morton(sources[2 * x], sources[2 * x + 1]) < morton(sources[2 * y], sources[2 * y + 1]);
-    });
+    for (int64_t k = 0; k < n; k++) all[k] = key[k].second;
     for (int64_t k = 0; k < nloc; k++) ord[k] = all[b + k];
     srt.resize(2 * nloc);
     std::vector<int32_t> perm(nloc);
