@@ -191,19 +191,30 @@ __global__ void __launch_bounds__(256) k_moments(const T *__restrict__ U, const 
   }
 }
 
-// sum the partials in CTA order; scale by h powers; write rows of the table
-__global__ void k_mom_reduce(const double *__restrict__ partial, int nblk, int64_t chunk, int64_t nvalid,
-                             double h, double *__restrict__ mom /* rows of this chunk */,
-                             const int32_t *__restrict__ dest /* nullable: also scatter row s to */,
-                             double *__restrict__ mom_all /* row dest[s] (N1 sorted chunks) */) {
-  int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+// sum the partials in a fixed order (deterministic, independent of chunking
+// and ranks): one warp per source, lane l sums the CTAs b = l, l + 32, ... in
+// increasing order, then a fixed shuffle tree; scale by h powers; write rows
+// of the table.  (Round 2: the one-thread-per-source loop over all CTAs took
+// 3.6 ms per chunk -- latency-bound with a few hundred threads -- i.e. 9 % of
+// a windowed c4 solve.)
+__global__ void __launch_bounds__(256) k_mom_reduce(const double *__restrict__ partial, int nblk, int64_t chunk,
+                                                    int64_t nvalid, double h, double *__restrict__ mom /* rows of this chunk */,
+                                                    const int32_t *__restrict__ dest /* nullable: also scatter row s to */,
+                                                    double *__restrict__ mom_all /* row dest[s] (N1 sorted chunks) */) {
+  const int lane = threadIdx.x & 31;
+  const int64_t s = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (s >= nvalid) return;
   double acc[6] = {0, 0, 0, 0, 0, 0};
-  for (int b = 0; b < nblk; b++) {
+  for (int b = lane; b < nblk; b += 32) {
     const double *p = partial + ((size_t)b * chunk + s) * 6;
 #pragma unroll
     for (int q = 0; q < 6; q++) acc[q] += p[q];
   }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+    for (int q = 0; q < 6; q++) acc[q] += __shfl_down_sync(0xffffffffu, acc[q], off);
+  if (lane != 0) return;
   const double h2 = h * h, h3 = h2 * h, h4 = h2 * h2;
   double *o = mom + s * 6;
   o[0] = acc[0] * h2;
@@ -1350,7 +1361,7 @@ after_stepping:
   dim3 mgrid(nblk, (ngroups + wpb - 1) / wpb);
   k_moments<T, NV, D2><<<mgrid, 32 * wpb, 0, st>>>(u, H->d_pix, H->d_src_xy, nact, ngroups, mpx, H->d_partial,
                                                chunk, H->windows ? H->d_grange : nullptr, H->momw);
-  k_mom_reduce<<<(int)((nvalid + 127) / 128), 128, 0, st>>>(H->d_partial, nblk, chunk, nvalid, H->h, mom_rows,
+  k_mom_reduce<<<(int)((nvalid + 7) / 8), 256, 0, st>>>(H->d_partial, nblk, chunk, nvalid, H->h, mom_rows,
                                                             H->windows ? H->d_perm + H->last_chunk_pos0 : nullptr,
                                                             H->d_mom);
   H->st.launches += 2;

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--windows", type=int, default=0)
     ap.add_argument("--precision", type=int, default=64)
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--diag", type=int, default=0, help="1: per-rank stage-kernel time / bytes / launches")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -35,14 +36,18 @@ def main():
     src = configs.sources(a.config)[:a.sources]
     dt = 1 / 32
     st = torch.cuda.current_stream()
+    diag_rows = []
 
     def run(r, R):
         with dg.Solver(m, 1.0, 1.0, 1, precision=a.precision, windows=a.windows, rank=r, nranks=R,
                        stream=st.cuda_stream) as s:
             s.solve(src, dt, 1)        # warm-up: kernels, tables and the full chunk buffers (allocated by solve)
+            if a.diag:                 # per-launch events: stage-kernel device time and bytes
+                dg.dgdiff_set_timing(s.handle, 1)
             best = None
             for _ in range(a.reps):    # min over repetitions (clock / power transients)
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                dg.dgdiff_reset_stats(s.handle)
                 torch.cuda.synchronize()
                 e0.record(st)
                 s.solve(src, dt, a.nsteps)
@@ -50,13 +55,22 @@ def main():
                 e1.record(st)
                 torch.cuda.synchronize()
                 t = e0.elapsed_time(e1)
-                best = t if best is None else min(best, t)
+                if best is None or t < best:
+                    best = t
+                    if a.diag:
+                        stt = s.stats()
+                        drow = {"stage_ms": stt["stage_ms"], "stage_launches": stt["stage_launches"],
+                                "stage_gb": stt["stage_bytes"] / 1e9, "launches": stt["launches"], "chunk": stt["chunk"]}
+            if a.diag:
+                diag_rows.append(drow)
             return best, mom, s
 
     t1, M1, _ = run(0, 1)
     with dg.Solver(m, 1.0, 1.0, 1, precision=a.precision, windows=a.windows) as s:
         S1, mu1 = s.covariance_table(M1)
+    d1 = diag_rows[-1:] if a.diag else []
     for R in (1, 2, 4, 8):
+        diag_rows.clear()
         times, tab = [], np.zeros_like(M1)
         for r in range(R):
             t, Mr, _ = run(r, R) if R > 1 else (t1, M1, None)
@@ -68,6 +82,7 @@ def main():
                           "precision": a.precision, "ranks": R, "rank_ms": times, "max_rank_ms": max(times),
                           "sum_rank_ms": sum(times), "projected_speedup": t1 / max(times),
                           "allreduce_bytes": int(len(src)) * 48,
+                          **({"diag": (d1 if R == 1 else list(diag_rows))} if a.diag else {}),
                           "bitwise_equal_to_one_rank": bool(np.array_equal(tab, M1) and np.array_equal(SR, S1)
                                                             and np.array_equal(muR, mu1))}), flush=True)
 
