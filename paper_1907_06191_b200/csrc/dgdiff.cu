@@ -444,6 +444,7 @@ struct dgdiff_s {
   void *d_U[3] = {nullptr, nullptr, nullptr};
   void *d_Ubase = nullptr;
   int64_t chunk_cap = 0;  // sources the U buffers hold
+  bool chunk_cap_fit = false;  // chunk_cap was limited by free device memory
   int *d_src_a = nullptr;
   int2 *d_src_ij = nullptr;
   double2 *d_src_xy = nullptr;   // source points, pixel units (per chunk slot)
@@ -1523,7 +1524,9 @@ static dgdiff_status solve_impl(dgdiff_s *H, const int32_t *sources, const doubl
     int64_t want = (nloc + G - 1) / G * G;
     int64_t chunk = want;
     if (H->o.max_chunk > 0) chunk = std::min<int64_t>(chunk, std::max<int64_t>(G, H->o.max_chunk / G * G));
-    if (chunk > H->chunk_cap) {
+    // (a capacity that free memory limited is kept: re-allocating ~150 GB of
+    // state on every solve larger than it cost ~0.13 s per call)
+    if (chunk > H->chunk_cap && !H->chunk_cap_fit) {
       cudaFree(H->d_Ubase);
       H->d_Ubase = nullptr;
       for (int r = 0; r < 3; r++) H->d_U[r] = nullptr;
@@ -1535,6 +1538,7 @@ static dgdiff_status solve_impl(dgdiff_s *H, const int32_t *sources, const doubl
       CK(cudaMemGetInfo(&fr, &tot));
       int64_t fit = (int64_t)((double)fr * 0.85 / (double)per_src) / G * G;
       if (fit < G) return fail(DGDIFF_E_NOMEM, "one source group (%d sources) needs %.3g GB", G, per_src * G / 1e9);
+      H->chunk_cap_fit = fit < chunk;
       chunk = std::min(chunk, fit);
       // the three RK registers live in one allocation; env DGDIFF_STAGGER=b
       // offsets register r by r*b extra bytes (layout experiments)
