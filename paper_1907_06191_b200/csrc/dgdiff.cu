@@ -1425,6 +1425,12 @@ static dgdiff_status solve_impl(dgdiff_s *H, const int32_t *sources, const doubl
   }
   CK(cudaSetDevice(H->dev));
   H->solved = false;
+  // no chunk of this solve kept yet (a rank whose shard is empty keeps none:
+  // dgdiff_get_density must not see the previous solve's chunk)
+  H->last_chunk_begin = -1;
+  H->last_chunk_n = 0;
+  H->last_chunk_pos0 = 0;
+  H->h_spos.clear();
   H->st.h2d_bytes = 0;
   H->st.d2h_bytes = 0;
   int64_t b, e;

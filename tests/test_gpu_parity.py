@@ -1061,3 +1061,32 @@ def test_q2_gamma_crop_full_bands_vs_oracle(dg, orc, cfg):
     assert mom_err(mom, ref_m) <= t["mom"]
     R, _ = orc.sigma(ref_m)
     assert sig_err(S, R) <= t["sig"]
+
+
+@pytest.mark.parametrize("windows", [0, 1])
+def test_logical_ranks_more_ranks_than_sources(dg, cfg, windows):
+    """R = 8 logical ranks for 3 sources: five ranks get an empty shard (a
+    zero table, no kept chunk: get_density refuses instead of returning an
+    earlier solve's state); the summed tables give one rank's Sigma bitwise."""
+    m = cfg.mask("c1")
+    src = np.array([[4, 16], [5, 16], [4, 17]], np.int32)
+    with dg.Solver(m, 1.0, 1.0, 1, windows=windows) as s:
+        s.solve(src, 1 / 32, 20)
+        S1, mu1 = s.covariance()
+        M1 = s.moments()
+    tab = np.zeros_like(M1)
+    for r in range(8):
+        with dg.Solver(m, 1.0, 1.0, 1, windows=windows, rank=r, nranks=8, keep_density=1) as s:
+            s.solve(np.repeat(src, 6, axis=0)[:16], 1 / 32, 4)   # earlier: every rank keeps a chunk
+            s.solve(src, 1 / 32, 20)
+            Mr = s.moments()
+            b, e = dg.dgdiff_shard(len(src), r, 8)
+            if e == b:
+                assert np.all(Mr == 0)
+                with pytest.raises(dg.DGDiffError):
+                    s.density(0)
+            tab += Mr
+            if r == 7:
+                SR, muR = s.covariance_table(tab)
+    assert np.array_equal(tab, M1)
+    assert np.array_equal(SR, S1) and np.array_equal(muR, mu1)
