@@ -255,6 +255,33 @@ def measure_k3d(args, dg, mask, batch, dt, nsteps, per_step, dofs, dist, stream,
         s.close()
 
 
+def measure_adjoint(args, dg, mask, all_src, dt, nsteps, stream, rank, world, local, peak_unused=None):
+    """Adjoint moments (opts.adjoint = 1) for the WHOLE source set of the
+    configuration (c4: all 65 536 sources) x nsteps: one solve + covariance,
+    timed with CUDA events after a warm-up; logical ranks take their shard
+    (no communicator here: this is a side measurement, Sigma from rank 0's
+    table when world == 1)."""
+    import torch
+    s = dg.Solver(mask, 1.0, 1.0, args.degree, adjoint=1, stream=stream.cuda_stream, device=local)
+    try:
+        s.solve(all_src[:64], dt, 1)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        s.solve(all_src, dt, nsteps)
+        S, _ = s.covariance()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        return {"sources": int(len(all_src)), "nsteps": nsteps, "ms": ms, "sigma_solves_per_s": 1e3 / ms,
+                "sigma": [S[0, 0], S[0, 1], S[1, 1]],
+                "note": "moments of every source from 3 source groups of weight fields stepped with the "
+                        "transposed operator (v1 table kernel) and read at each source pixel; the same Sigma as "
+                        "the per-source solves of the whole job up to rounding (DESIGN 9b, N5)"}
+    finally:
+        s.close()
+
+
 def run_ours(args):
     import torch
     world, rank, local = dist_env()
@@ -376,6 +403,8 @@ def run_ours(args):
     if args.temporal_steps == 0 and args.degree == 1 and not args.windows and args.k3d_steps > 0:
         line["k3d"] = measure_k3d(args, dg, mask, batch, dt, nsteps, per_step, dofs, dist, stream, rank, world,
                                   local, nccl_id, peak)
+    if rank == 0 and world == 1 and args.precision == 64 and not args.windows and args.adjoint_job:
+        line["adjoint_full_job"] = measure_adjoint(args, dg, mask, all_src, dt, nsteps, stream, rank, world, local)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(mask, all_src, args.degree)
     if rank == 0:
@@ -394,6 +423,8 @@ def main():
     ap.add_argument("--precision", type=int, default=64, choices=[64, 32])
     ap.add_argument("--degree", type=int, default=1, choices=[1, 2])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--adjoint-job", type=int, default=1,
+                    help="1: also time the adjoint-moment solve of the whole source set (Sigma of the full job)")
     ap.add_argument("--k3d-steps", type=int, default=3,
                     help="extra K3d steps timed beside the default K2 line (0 = skip)")
     ap.add_argument("--temporal-steps", type=int, default=DEFAULT_TS, choices=[0, 5],

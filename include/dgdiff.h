@@ -133,6 +133,23 @@ typedef struct {
                              composite operator is a 9-point cross.  Default
                              ring kernel only (REFLECT or ABSORB); densities
                              are [ny][nx][(p+1)^2] */
+  int32_t adjoint;        /* 1 = moments by the adjoint (round 2): for the
+                             linear scheme m_s = w_s^T P(dt L)^N u0_s =
+                             (P(dt L^T)^N w_s)^T u0_s, and the moment weights
+                             w_s about the source point are combinations of the
+                             six weight fields of 1, x, y, x^2, xy, y^2 about a
+                             nearby origin; so dgdiff_solve_batch evolves those
+                             fields (30 origins on a lattice over the sources'
+                             box: 180 lanes of three 64-lane groups) with the
+                             transposed composite operator (v1 table kernel)
+                             and reads every source's moments from them at its
+                             pixel: three groups of work for any number of
+                             sources.  Same Sigma as the
+                             per-source solve up to rounding (the centring
+                             subtraction loses ~log10(box^2 / m_20) digits).
+                             fp64, P1/P2 triangles, REFLECT, no windows,
+                             mixture, temporal blocking or densities (E_ARG);
+                             0 (default) = per-source forward solves */
 } dgdiff_opts;
 
 /* Fill *o with the defaults above. */

@@ -231,6 +231,92 @@ __global__ void __launch_bounds__(256) k_mom_reduce(const double *__restrict__ p
 }
 
 // ---------------------------------------------------------------------------
+// Adjoint moments (opts.adjoint, round 2).  The scheme is linear, so a
+// source's moment m = w_s^T P(dt L)^N u0_s equals (P(dt L^T)^N w_s)^T u0_s,
+// and the weights w_s of (x - x_s)^a (y - y_s)^b are combinations of the six
+// weight fields of 1, x', y', x'^2, x'y', y'^2 (x' = x - x_o about an origin
+// o).  k_adj_init writes those fields for AO origins into lanes 6 o + q of one
+// source group (the other lanes zero); the stages then run with the
+// transposed table; k_adj_eval reads each source's six values at its pixel
+// (against the projected Dirac, as K4 integrates a density) and re-centres
+// them on the source point.
+// ---------------------------------------------------------------------------
+constexpr int ADJ_GROUPS = 3;                  // source groups of adjoint fields
+constexpr int ADJ_PER_GROUP = 10;              // origins per 64-lane group (6 lanes each)
+constexpr int ADJ_MAXO = ADJ_GROUPS * ADJ_PER_GROUP;
+struct AdjOrigins { double x[ADJ_MAXO], y[ADJ_MAXO]; int n; };
+
+template <int D2>
+__global__ void k_adj_init(double *__restrict__ U, const int2 *__restrict__ pix, int nact, double h, MomW mw,
+                           AdjOrigins org) {
+  constexpr int G = 64, d = D2 / 2;
+  const int64_t per_group = (int64_t)nact * D2 * G;
+  const int64_t total = per_group * ADJ_GROUPS;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int lane = (int)(idx % G);
+    const int k = (int)((idx / G) % D2);
+    const int a = (int)((idx % per_group) / ((int64_t)G * D2));
+    const int gi = (int)(idx / per_group);
+    const int o = lane / 6 < ADJ_PER_GROUP ? gi * ADJ_PER_GROUP + lane / 6 : ADJ_MAXO, q = lane % 6;
+    double v = 0.0;
+    if (o < org.n) {
+      const int t = k / d, jl = k % d;
+      const int2 ij = __ldg(&pix[a]);
+      const double X = ij.x - org.x[o], Y = ij.y - org.y[o];
+      const double *w = mw.w + t * 6 * DMAXK + jl;   // unit-pixel integrals of xi^a eta^b N_jl
+      const double w00 = w[0], w10 = w[DMAXK], w01 = w[2 * DMAXK], w20 = w[3 * DMAXK], w11 = w[4 * DMAXK],
+                   w02 = w[5 * DMAXK];
+      const double h2 = h * h, h3 = h2 * h, h4 = h2 * h2;
+      v = q == 0 ? h2 * w00
+        : q == 1 ? h3 * (w10 + X * w00)
+        : q == 2 ? h3 * (w01 + Y * w00)
+        : q == 3 ? h4 * (w20 + 2.0 * X * w10 + X * X * w00)
+        : q == 4 ? h4 * (w11 + X * w01 + Y * w10 + X * Y * w00)
+                 : h4 * (w02 + 2.0 * Y * w01 + Y * Y * w00);
+    }
+    U[idx] = v;
+  }
+}
+
+template <int D2>
+__global__ void k_adj_eval(const double *__restrict__ U, int nact, const int32_t *__restrict__ src, int64_t b, int64_t nloc,
+                           const int *__restrict__ aidx, int nx, double h, InitVals iv, AdjOrigins org,
+                           double *__restrict__ mom) {
+  constexpr int G = 64;
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= nloc) return;
+  const int64_t s = b + k;
+  const int i = src[2 * s], j = src[2 * s + 1];
+  const int a = __ldg(&aidx[(size_t)j * nx + i]);
+  const double xs = i + 0.5, ys = j + 0.5;
+  int o = 0;
+  double best = 1e300;
+  for (int c = 0; c < org.n; c++) {
+    const double dx = xs - org.x[c], dy = ys - org.y[c], r = dx * dx + dy * dy;
+    if (r < best) { best = r; o = c; }
+  }
+  double E[6];
+#pragma unroll
+  for (int q = 0; q < 6; q++) {
+    double e = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < D2; kk++)
+      e = fma(U[(size_t)(o / ADJ_PER_GROUP) * nact * D2 * G + ((size_t)a * D2 + kk) * G + 6 * (o % ADJ_PER_GROUP) + q],
+              iv.v[kk], e);
+    E[q] = e;
+  }
+  const double dX = h * (xs - org.x[o]), dY = h * (ys - org.y[o]);
+  double *m = mom + s * 6;
+  m[0] = E[0];
+  m[1] = E[1] - dX * E[0];
+  m[2] = E[2] - dY * E[0];
+  m[3] = E[3] - 2.0 * dX * E[1] + dX * dX * E[0];
+  m[4] = E[4] - dX * E[2] - dY * E[1] + dX * dY * E[0];
+  m[5] = E[5] - 2.0 * dY * E[2] + dY * dY * E[0];
+}
+
+// ---------------------------------------------------------------------------
 // K5: mixture and its covariance from the full
 // [n][6] table, fixed-order reduction (bitwise identical on every rank).
 // out[0..5] = sxx sxy syy mux muy flags (bit0 degenerate, bit1 non-finite)
@@ -932,6 +1018,24 @@ static dgdiff_status create_impl(dgdiff_s *H, const uint8_t *mask) {
     for (size_t k = 0; k < na; k++) A32[k] = (float)H->tab.A[k];
     CK(cudaMalloc(&H->d_A, na * sizeof(float)));
     CK(cudaMemcpy(H->d_A, A32.data(), na * sizeof(float), cudaMemcpyHostToDevice));
+  } else if (H->o.adjoint) {
+    // the transposed composite operator L^T for the adjoint fields: the self
+    // block of code c transposed; the block coupling a pixel to its
+    // neighbour across open face f is [L_{q,p}]^T = (N_opp(f))^T (the shared
+    // face is open from both sides, so q's block for p is the fixed N)
+    const int D2 = 2 * H->tab.d;
+    std::vector<double> AT(na, 0.0);
+    auto Ai = [&](int code, int o, int r, int c) { return ((size_t)(code * 5 + o) * D2 + r) * D2 + c; };
+    const int opp[5] = {0, 2, 1, 4, 3};
+    for (int code = 0; code < 16; code++)
+      for (int r = 0; r < D2; r++)
+        for (int c = 0; c < D2; c++) {
+          AT[Ai(code, 0, r, c)] = H->tab.A[Ai(code, 0, c, r)];
+          for (int f = 1; f <= 4; f++)
+            if ((code >> (f - 1)) & 1) AT[Ai(code, f, r, c)] = H->tab.A[Ai(15, opp[f], c, r)];
+        }
+    CK(cudaMalloc(&H->d_A, na * sizeof(double)));
+    CK(cudaMemcpy(H->d_A, AT.data(), na * sizeof(double), cudaMemcpyHostToDevice));
   } else {
     CK(cudaMalloc(&H->d_A, na * sizeof(double)));
     CK(cudaMemcpy(H->d_A, H->tab.A.data(), na * sizeof(double), cudaMemcpyHostToDevice));
@@ -1043,6 +1147,13 @@ extern "C" dgdiff_status dgdiff_create(dgdiff_t *out, const uint8_t *mask, int32
   if (o.kernel < 0 || o.kernel > 3) return fail(DGDIFF_E_ARG, "kernel must be 0..3");
   if (o.max_chunk < 0) return fail(DGDIFF_E_ARG, "max_chunk < 0");
   if (o.mixture_radius < 0 || o.mixture_radius > 2048) return fail(DGDIFF_E_ARG, "mixture_radius must be in [0, 2048]");
+  if (o.adjoint != 0 && o.adjoint != 1) return fail(DGDIFF_E_ARG, "adjoint must be 0 or 1");
+  if (o.adjoint == 1 && (o.precision != 64 || degree > 2 || o.element != 0 || o.outer_bc != 0 || o.windows != 0 ||
+                         o.temporal_steps > 1 || o.kernel == 2 || o.kernel == 3 || o.mixture_radius != 0 ||
+                         o.keep_density != 0))
+    return fail(DGDIFF_E_ARG, "adjoint moments: fp64 P1/P2 triangles, REFLECT, no windows / temporal blocking / "
+                              "mixture / densities");
+  if (o.adjoint == 1) o.kernel = 1;   // the adjoint fields step on the v1 table kernel (transposed table)
   dgdiff_s *H = new dgdiff_s();
   H->nx = nx; H->ny = ny; H->h = h; H->D = D; H->p = degree;
   H->d = (degree + 1) * (degree + 2) / 2;
@@ -1402,6 +1513,103 @@ static dgdiff_status run_chunk_p(dgdiff_s *H, int64_t nvalid, int64_t chunk, dou
   return fail(DGDIFF_E_ARG, "internal: lane width");
 }
 
+// Adjoint moments (opts.adjoint): see k_adj_init.  ADJ_GROUPS 64-lane groups
+// of weight fields about up to 30 origins (a lattice over the box of this
+// rank's sources, so that |x_s - x_o| stays small and the re-centring
+// subtraction loses few digits: with 9 origins the worst c4 source's second
+// moments differed from the per-source solve by 1.4e-10), stepped with the
+// transposed operator, then every source of the shard [b, b + nloc) is
+// evaluated into its table row.
+template <int D2>
+static dgdiff_status adjoint_solve(dgdiff_s *H, const int32_t *sources, int64_t b, int64_t nloc, double dt,
+                                   int64_t nsteps) {
+  constexpr int G = 64;
+  const int P = D2 == 6 ? 1 : 2;
+  const int nact = (int)H->nact;
+  cudaStream_t st = H->stream;
+  if (H->chunk_cap < ADJ_GROUPS * G) {
+    cudaFree(H->d_Ubase);
+    H->d_Ubase = nullptr;
+    const size_t reg = (size_t)nact * D2 * G * ADJ_GROUPS * sizeof(double);
+    CK(cudaMalloc(&H->d_Ubase, 3 * reg));
+    for (int r = 0; r < 3; r++) H->d_U[r] = (char *)H->d_Ubase + r * reg;
+    H->chunk_cap = ADJ_GROUPS * G;
+    H->chunk_cap_fit = false;
+  }
+  AdjOrigins org;
+  org.n = 0;
+  if (nloc > 0) {
+    int x0 = INT32_MAX, x1 = INT32_MIN, y0 = INT32_MAX, y1 = INT32_MIN;
+    for (int64_t k = 0; k < nloc; k++) {
+      x0 = std::min(x0, sources[2 * (b + k)]);
+      x1 = std::max(x1, sources[2 * (b + k)]);
+      y0 = std::min(y0, sources[2 * (b + k) + 1]);
+      y1 = std::max(y1, sources[2 * (b + k) + 1]);
+    }
+    // a kx x ky lattice of cell centres (kx ky <= ADJ_MAXO), cells as square
+    // as the box allows
+    const double wx = x1 + 1 - x0, wy = y1 + 1 - y0;
+    int kx = 1, ky = 1;
+    for (int cx = 1; cx <= ADJ_MAXO; cx++) {
+      const int cy = ADJ_MAXO / cx;
+      if (cy < 1) break;
+      if (std::max(wx / cx, wy / cy) < std::max(wx / kx, wy / ky)) { kx = cx; ky = cy; }
+    }
+    for (int oy = 0; oy < ky; oy++)
+      for (int ox = 0; ox < kx; ox++) {
+        org.x[org.n] = x0 + wx * (2 * ox + 1) / (2.0 * kx);
+        org.y[org.n] = y0 + wy * (2 * oy + 1) / (2.0 * ky);
+        org.n++;
+      }
+  }
+  double *u = (double *)H->d_U[0], *Ua = (double *)H->d_U[1], *Ub = (double *)H->d_U[2];
+  const int64_t total = (int64_t)nact * D2 * G * ADJ_GROUPS;
+  k_adj_init<D2><<<(int)std::min<int64_t>((total + 255) / 256, 148 * 64), 256, 0, st>>>(u, H->d_pix, nact, H->h,
+                                                                                           H->momw, org);
+  H->st.launches++;
+  dgl::StageArgs sa;
+  sa.nbr = H->d_nbr;
+  sa.A = H->d_A;          // the transposed table (dgdiff_create, adjoint)
+  sa.nact = nact;
+  sa.ny = H->ny;
+  sa.ngroups = ADJ_GROUPS;
+  sa.nsm = H->nsm;
+  sa.px = 32;
+  sa.wpb = std::min(ADJ_GROUPS, 4);
+  sa.st = st;
+  const double c = dt * H->D / (H->h * H->h);
+  auto stage = [&](const double *Uin, double *Uout, double alpha, double cs) -> dgdiff_status {
+    sa.Uin = Uin;
+    sa.U0 = u;
+    sa.Uout = Uout;
+    sa.alpha = alpha;
+    sa.cs = cs;
+    cudaError_t e = dgl::launch_stage(0, 64, P, alpha != 0.0, sa);
+    if (e != cudaSuccess) return fail(DGDIFF_E_CUDA, "adjoint stage launch: %s", cudaGetErrorString(e));
+    return DGDIFF_OK;
+  };
+  for (int64_t step = 0; step < nsteps; step++) {   // SSP-RK3 increment form, as run_chunk
+    dgdiff_status r;
+    if ((r = stage(u, Ua, 0.0, c)) != DGDIFF_OK) return r;
+    if ((r = stage(Ua, Ub, 0.75, 0.25 * c)) != DGDIFF_OK) return r;
+    if ((r = stage(Ub, u, 1.0 / 3.0, (2.0 / 3.0) * c)) != DGDIFF_OK) return r;
+  }
+  H->st.launches += 3 * nsteps;
+  H->st.stage_launches += 3 * nsteps;
+  H->st.stage_bytes += 8.0 * (double)nact * D2 * G * ADJ_GROUPS * sizeof(double) * nsteps;
+  if (nloc > 0) {
+    InitVals iv;
+    const double ih2 = 1.0 / (H->h * H->h);
+    for (int k = 0; k < D2; k++) iv.v[k] = H->tab.init[k] * ih2;
+    k_adj_eval<D2><<<(int)((nloc + 127) / 128), 128, 0, st>>>(u, nact, H->d_src, b, nloc, H->d_aidx, H->nx, H->h, iv, org,
+                                                              H->d_mom);
+    H->st.launches++;
+  }
+  CK(cudaGetLastError());
+  H->st.chunk = ADJ_GROUPS * G;
+  return DGDIFF_OK;
+}
+
 // sources: [n][2] pixel (i, j); px: nullable [n][2 + D2] sub-pixel points
 // (pixel units) and their projected-Dirac rows (N4), in the same order
 static dgdiff_status solve_impl(dgdiff_s *H, const int32_t *sources, const double *px, int64_t n, double dt,
@@ -1464,6 +1672,17 @@ static dgdiff_status solve_impl(dgdiff_s *H, const int32_t *sources, const doubl
   H->h_src_stage.assign(sources, sources + 2 * n);
   CK(cudaMemcpyAsync(H->d_src, H->h_src_stage.data(), sizeof(int32_t) * 2 * n, cudaMemcpyHostToDevice, H->stream));
   H->st.h2d_bytes += sizeof(int32_t) * 2 * n;
+  if (H->o.adjoint) {
+    if (px) return fail(DGDIFF_E_ARG, "adjoint moments: pixel sources only");
+    dgdiff_status r = H->D2 == 6 ? adjoint_solve<6>(H, sources, b, nloc, dt, nsteps)
+                                 : adjoint_solve<12>(H, sources, b, nloc, dt, nsteps);
+    if (r != DGDIFF_OK) return r;
+    H->solved = true;
+    H->last_n = n;
+    H->last_dt = dt;
+    H->last_nsteps = nsteps;
+    return DGDIFF_OK;
+  }
   std::vector<int32_t> srt;   // N1: this rank's sources in Morton order
   // chunk order -> global source index: the contiguous shard [b, e), or under
   // N1 windows the shard [b, e) of the WHOLE batch in Morton order (every rank

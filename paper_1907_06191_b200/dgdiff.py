@@ -36,7 +36,7 @@ class dgdiff_opts(ctypes.Structure):
                 ("nranks", ctypes.c_int32), ("nccl_id", ctypes.c_void_p), ("keep_density", ctypes.c_int32),
                 ("max_chunk", ctypes.c_int32), ("stream", ctypes.c_void_p), ("kernel", ctypes.c_int32),
                 ("mixture_radius", ctypes.c_int32), ("windows", ctypes.c_int32),
-                ("element", ctypes.c_int32)]
+                ("element", ctypes.c_int32), ("adjoint", ctypes.c_int32)]
 
 
 class dgdiff_stats_t(ctypes.Structure):
