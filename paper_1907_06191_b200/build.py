@@ -28,7 +28,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES = ["dgdiff.cu", "launch.cu", "stage_v12_f64.cu", "stage_v12_f32.cu", "stage_ring_p1_f64.cu",
            "stage_ring_p1_f32.cu", "stage_ring_p2_f64.cu", "stage_ring_p2_f32.cu",
            "stage_ring_p3_f64.cu", "stage_ring_p3_f32.cu", "stage_ring_q_f64.cu", "stage_ring_q_f32.cu", "step_fused_f64.cu", "step_dec_f64.cu", "step_wave.cu",
-           "step_fused_f32.cu", "stage_pair.cu", "operator.cpp"]
+           "step_fused_f32.cu", "stage_pair.cu", "stage_ring_adj_f64.cu", "operator.cpp"]
 HEADERS = ["kernels.cuh", "operator.h", "stage_imm.cuh", "stage_ring.cuh", "stage_v12.cuh", "launch.h",
            "step_fused.cuh", "step_dec.cuh", "stage_wave.cuh", "mc_walk.cuh", "stage_pair.cuh"]
 OBJDIR = os.path.join(HERE, "build_obj")

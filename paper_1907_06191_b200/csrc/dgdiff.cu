@@ -241,24 +241,24 @@ __global__ void __launch_bounds__(256) k_mom_reduce(const double *__restrict__ p
 // (against the projected Dirac, as K4 integrates a density) and re-centres
 // them on the source point.
 // ---------------------------------------------------------------------------
-constexpr int ADJ_GROUPS = 3;                  // source groups of adjoint fields
-constexpr int ADJ_PER_GROUP = 10;              // origins per 64-lane group (6 lanes each)
-constexpr int ADJ_MAXO = ADJ_GROUPS * ADJ_PER_GROUP;
+constexpr int ADJ_MAXO = 30;                   // origins (6 field lanes each)
+template <int G> __host__ __device__ constexpr int adj_per_group() { return G / 6; }
+template <int G> __host__ __device__ constexpr int adj_groups() { return (ADJ_MAXO + G / 6 - 1) / (G / 6); }
 struct AdjOrigins { double x[ADJ_MAXO], y[ADJ_MAXO]; int n; };
 
-template <int D2>
+template <int D2, int G>
 __global__ void k_adj_init(double *__restrict__ U, const int2 *__restrict__ pix, int nact, double h, MomW mw,
                            AdjOrigins org) {
-  constexpr int G = 64, d = D2 / 2;
+  constexpr int d = D2 / 2, OPG = adj_per_group<G>();
   const int64_t per_group = (int64_t)nact * D2 * G;
-  const int64_t total = per_group * ADJ_GROUPS;
+  const int64_t total = per_group * adj_groups<G>();
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int lane = (int)(idx % G);
     const int k = (int)((idx / G) % D2);
     const int a = (int)((idx % per_group) / ((int64_t)G * D2));
     const int gi = (int)(idx / per_group);
-    const int o = lane / 6 < ADJ_PER_GROUP ? gi * ADJ_PER_GROUP + lane / 6 : ADJ_MAXO, q = lane % 6;
+    const int o = lane / 6 < OPG ? gi * OPG + lane / 6 : ADJ_MAXO, q = lane % 6;
     double v = 0.0;
     if (o < org.n) {
       const int t = k / d, jl = k % d;
@@ -279,11 +279,11 @@ __global__ void k_adj_init(double *__restrict__ U, const int2 *__restrict__ pix,
   }
 }
 
-template <int D2>
+template <int D2, int G>
 __global__ void k_adj_eval(const double *__restrict__ U, int nact, const int32_t *__restrict__ src, int64_t b, int64_t nloc,
                            const int *__restrict__ aidx, int nx, double h, InitVals iv, AdjOrigins org,
                            double *__restrict__ mom) {
-  constexpr int G = 64;
+  constexpr int OPG = adj_per_group<G>();
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= nloc) return;
   const int64_t s = b + k;
@@ -302,8 +302,7 @@ __global__ void k_adj_eval(const double *__restrict__ U, int nact, const int32_t
     double e = 0.0;
 #pragma unroll
     for (int kk = 0; kk < D2; kk++)
-      e = fma(U[(size_t)(o / ADJ_PER_GROUP) * nact * D2 * G + ((size_t)a * D2 + kk) * G + 6 * (o % ADJ_PER_GROUP) + q],
-              iv.v[kk], e);
+      e = fma(U[(size_t)(o / OPG) * nact * D2 * G + ((size_t)a * D2 + kk) * G + 6 * (o % OPG) + q], iv.v[kk], e);
     E[q] = e;
   }
   const double dX = h * (xs - org.x[o]), dY = h * (ys - org.y[o]);
@@ -1153,7 +1152,6 @@ extern "C" dgdiff_status dgdiff_create(dgdiff_t *out, const uint8_t *mask, int32
                          o.keep_density != 0))
     return fail(DGDIFF_E_ARG, "adjoint moments: fp64 P1/P2 triangles, REFLECT, no windows / temporal blocking / "
                               "mixture / densities");
-  if (o.adjoint == 1) o.kernel = 1;   // the adjoint fields step on the v1 table kernel (transposed table)
   dgdiff_s *H = new dgdiff_s();
   H->nx = nx; H->ny = ny; H->h = h; H->D = D; H->p = degree;
   H->d = (degree + 1) * (degree + 2) / 2;
@@ -1513,31 +1511,38 @@ static dgdiff_status run_chunk_p(dgdiff_s *H, int64_t nvalid, int64_t chunk, dou
   return fail(DGDIFF_E_ARG, "internal: lane width");
 }
 
-// Adjoint moments (opts.adjoint): see k_adj_init.  ADJ_GROUPS 64-lane groups
-// of weight fields about up to 30 origins (a lattice over the box of this
-// rank's sources, so that |x_s - x_o| stays small and the re-centring
-// subtraction loses few digits: with 9 origins the worst c4 source's second
-// moments differed from the per-source solve by 1.4e-10), stepped with the
-// transposed operator, then every source of the shard [b, b + nloc) is
-// evaluated into its table row.
-template <int D2>
+// Adjoint moments (opts.adjoint): see k_adj_init.  The weight fields of up to
+// 30 origins (a lattice over the box of this rank's sources, so that
+// |x_s - x_o| stays small and the re-centring subtraction loses few digits:
+// with 9 origins the worst c4 source's second moments differed from the
+// per-source solve by 1.4e-10) fill ceil(30 / (G / 6)) source groups; they
+// step with the transposed operator -- on the ring kernel with transposed
+// compile-time tables (default), restricted to the sources' domain of
+// dependence (stage k of the 3N computes only the box grown by 3N - 1 - k
+// pixels: nothing outside can reach a source pixel by the end; pixels outside
+// keep stale values that are never read), or on the v1 table kernel with the
+// transposed table (opts.kernel = 1) -- then every source of the shard
+// [b, b + nloc) is evaluated into its table row.
+template <int D2, int G>
 static dgdiff_status adjoint_solve(dgdiff_s *H, const int32_t *sources, int64_t b, int64_t nloc, double dt,
                                    int64_t nsteps) {
-  constexpr int G = 64;
+  constexpr int NG = adj_groups<G>();
   const int P = D2 == 6 ? 1 : 2;
   const int nact = (int)H->nact;
+  const bool ring = use_ring(H);
   cudaStream_t st = H->stream;
-  if (H->chunk_cap < ADJ_GROUPS * G) {
+  if (H->chunk_cap < NG * G) {
     cudaFree(H->d_Ubase);
     H->d_Ubase = nullptr;
-    const size_t reg = (size_t)nact * D2 * G * ADJ_GROUPS * sizeof(double);
+    const size_t reg = (size_t)nact * D2 * G * NG * sizeof(double);
     CK(cudaMalloc(&H->d_Ubase, 3 * reg));
     for (int r = 0; r < 3; r++) H->d_U[r] = (char *)H->d_Ubase + r * reg;
-    H->chunk_cap = ADJ_GROUPS * G;
+    H->chunk_cap = NG * G;
     H->chunk_cap_fit = false;
   }
   AdjOrigins org;
   org.n = 0;
+  int4 box = make_int4(0, H->nx - 1, 0, H->ny - 1);
   if (nloc > 0) {
     int x0 = INT32_MAX, x1 = INT32_MIN, y0 = INT32_MAX, y1 = INT32_MIN;
     for (int64_t k = 0; k < nloc; k++) {
@@ -1546,6 +1551,7 @@ static dgdiff_status adjoint_solve(dgdiff_s *H, const int32_t *sources, int64_t 
       y0 = std::min(y0, sources[2 * (b + k) + 1]);
       y1 = std::max(y1, sources[2 * (b + k) + 1]);
     }
+    box = make_int4(x0, x1, y0, y1);
     // a kx x ky lattice of cell centres (kx ky <= ADJ_MAXO), cells as square
     // as the box allows
     const double wx = x1 + 1 - x0, wy = y1 + 1 - y0;
@@ -1563,28 +1569,54 @@ static dgdiff_status adjoint_solve(dgdiff_s *H, const int32_t *sources, int64_t 
       }
   }
   double *u = (double *)H->d_U[0], *Ua = (double *)H->d_U[1], *Ub = (double *)H->d_U[2];
-  const int64_t total = (int64_t)nact * D2 * G * ADJ_GROUPS;
-  k_adj_init<D2><<<(int)std::min<int64_t>((total + 255) / 256, 148 * 64), 256, 0, st>>>(u, H->d_pix, nact, H->h,
-                                                                                           H->momw, org);
+  const int64_t total = (int64_t)nact * D2 * G * NG;
+  k_adj_init<D2, G><<<(int)std::min<int64_t>((total + 255) / 256, 148 * 64), 256, 0, st>>>(u, H->d_pix, nact, H->h,
+                                                                                              H->momw, org);
   H->st.launches++;
   dgl::StageArgs sa;
   sa.nbr = H->d_nbr;
-  sa.A = H->d_A;          // the transposed table (dgdiff_create, adjoint)
+  sa.A = H->d_A;          // v1: the transposed table (dgdiff_create, adjoint)
   sa.nact = nact;
   sa.ny = H->ny;
-  sa.ngroups = ADJ_GROUPS;
+  sa.ngroups = NG;
   sa.nsm = H->nsm;
   sa.px = 32;
-  sa.wpb = std::min(ADJ_GROUPS, 4);
+  sa.wpb = std::min(NG, 4);
   sa.st = st;
+  if (ring) {
+    sa.rowtab = H->d_rowtab;
+    sa.nstrips = H->nstrips;
+    sa.rowtab_na = H->d_rowtab_na;
+    sa.nstrips_na = H->nstrips_na;
+    sa.n1_use = H->n1_use;
+    sa.n1_use_na = H->n1_use > 0 ? H->n1_use : (int)(8.0 * H->mean_tile + 0.5);
+    sa.n2_use = H->n2_use;
+    // every group clips to the sources' box grown by the remaining reach
+    std::vector<int4> gb(NG, box);
+    if (NG > H->gbox_cap) {
+      cudaFree(H->d_gbox);
+      cudaFree(H->d_grange);
+      H->d_gbox = nullptr;
+      H->d_grange = nullptr;
+      CK(cudaMalloc(&H->d_gbox, sizeof(int4) * NG));
+      CK(cudaMalloc(&H->d_grange, sizeof(int2) * NG));
+      H->gbox_cap = NG;
+    }
+    CK(cudaMemcpyAsync(H->d_gbox, gb.data(), sizeof(int4) * NG, cudaMemcpyHostToDevice, st));
+    sa.gbox = H->d_gbox;
+    sa.band_rows = H->wband;
+  }
   const double c = dt * H->D / (H->h * H->h);
+  int64_t kst = 0;   // global stage index 0 .. 3N - 1
   auto stage = [&](const double *Uin, double *Uout, double alpha, double cs) -> dgdiff_status {
     sa.Uin = Uin;
     sa.U0 = u;
     sa.Uout = Uout;
     sa.alpha = alpha;
     sa.cs = cs;
-    cudaError_t e = dgl::launch_stage(0, 64, P, alpha != 0.0, sa);
+    sa.wr = (int)std::min<int64_t>(1 << 30, H->halo * (3 * nsteps - 1 - kst));
+    kst++;
+    cudaError_t e = ring ? dgl::launch_ring_adj_f64(P, alpha != 0.0, sa) : dgl::launch_stage(0, 64, P, alpha != 0.0, sa);
     if (e != cudaSuccess) return fail(DGDIFF_E_CUDA, "adjoint stage launch: %s", cudaGetErrorString(e));
     return DGDIFF_OK;
   };
@@ -1596,17 +1628,16 @@ static dgdiff_status adjoint_solve(dgdiff_s *H, const int32_t *sources, int64_t 
   }
   H->st.launches += 3 * nsteps;
   H->st.stage_launches += 3 * nsteps;
-  H->st.stage_bytes += 8.0 * (double)nact * D2 * G * ADJ_GROUPS * sizeof(double) * nsteps;
   if (nloc > 0) {
     InitVals iv;
     const double ih2 = 1.0 / (H->h * H->h);
     for (int k = 0; k < D2; k++) iv.v[k] = H->tab.init[k] * ih2;
-    k_adj_eval<D2><<<(int)((nloc + 127) / 128), 128, 0, st>>>(u, nact, H->d_src, b, nloc, H->d_aidx, H->nx, H->h, iv, org,
-                                                              H->d_mom);
+    k_adj_eval<D2, G><<<(int)((nloc + 127) / 128), 128, 0, st>>>(u, nact, H->d_src, b, nloc, H->d_aidx, H->nx, H->h,
+                                                                 iv, org, H->d_mom);
     H->st.launches++;
   }
   CK(cudaGetLastError());
-  H->st.chunk = ADJ_GROUPS * G;
+  H->st.chunk = NG * G;
   return DGDIFF_OK;
 }
 
@@ -1674,8 +1705,11 @@ static dgdiff_status solve_impl(dgdiff_s *H, const int32_t *sources, const doubl
   H->st.h2d_bytes += sizeof(int32_t) * 2 * n;
   if (H->o.adjoint) {
     if (px) return fail(DGDIFF_E_ARG, "adjoint moments: pixel sources only");
-    dgdiff_status r = H->D2 == 6 ? adjoint_solve<6>(H, sources, b, nloc, dt, nsteps)
-                                 : adjoint_solve<12>(H, sources, b, nloc, dt, nsteps);
+    const int G = gsize(H);
+    dgdiff_status r = H->D2 == 6 ? (G == 64 ? adjoint_solve<6, 64>(H, sources, b, nloc, dt, nsteps)
+                                            : adjoint_solve<6, 32>(H, sources, b, nloc, dt, nsteps))
+                                 : (G == 64 ? adjoint_solve<12, 64>(H, sources, b, nloc, dt, nsteps)
+                                            : adjoint_solve<12, 32>(H, sources, b, nloc, dt, nsteps));
     if (r != DGDIFF_OK) return r;
     H->solved = true;
     H->last_n = n;

@@ -136,19 +136,26 @@ static int emit(FILE *f, int p) {
     fprintf(f, "// nnz(P3) = %d\n\n", nnz);
     return emit_p3_columns(f, blk, D2);
   }
-  fprintf(f, "__host__ __device__ constexpr double tab_p%d(int b, int r, int c) {\n  switch ((b * %d + r) * %d + c) {\n", p, D2, D2);
-  int nnz = 0;
-  for (int b = 0; b < NB; b++)
-    for (int r = 0; r < D2; r++)
-      for (int c = 0; c < D2; c++) {
-        double v = blk[((size_t)b * D2 + r) * D2 + c];
-        if (v != 0.0) {
-          fprintf(f, "    case %d: return %a;\n", (b * D2 + r) * D2 + c, v);
-          nnz++;
+  // the transposed operator L^T (adjoint moments, opts.adjoint) has the same
+  // structure: self blocks transposed, and the block across open face f is the
+  // transposed neighbour block of the OPPOSITE face, (N_opp(f))^T
+  for (int tr = 0; tr < 2; tr++) {
+    fprintf(f, "__host__ __device__ constexpr double tab_p%d%s(int b, int r, int c) {\n  switch ((b * %d + r) * %d + c) {\n",
+            p, tr ? "t" : "", D2, D2);
+    int nnz = 0;
+    for (int b = 0; b < NB; b++)
+      for (int r = 0; r < D2; r++)
+        for (int c = 0; c < D2; c++) {
+          const int bs = (tr && b >= 5 && b <= 8) ? 5 + ((b - 5) ^ 1) : b;   // E<->W, N<->S
+          double v = tr ? blk[((size_t)bs * D2 + c) * D2 + r] : blk[((size_t)b * D2 + r) * D2 + c];
+          if (v != 0.0) {
+            fprintf(f, "    case %d: return %a;\n", (b * D2 + r) * D2 + c, v);
+            nnz++;
+          }
         }
-      }
-  fprintf(f, "    default: return 0.0;\n  }\n}\n");
-  fprintf(f, "// nnz(P%d) = %d\n\n", p, nnz);
+    fprintf(f, "    default: return 0.0;\n  }\n}\n");
+    fprintf(f, "// nnz(P%d%s) = %d\n\n", p, tr ? "t" : "", nnz);
+  }
   return 0;
 }
 

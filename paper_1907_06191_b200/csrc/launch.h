@@ -77,6 +77,8 @@ cudaError_t launch_ring_p2_f32(bool alpha, const StageArgs &a);
 cudaError_t launch_ring_p3_f64(bool alpha, const StageArgs &a);
 cudaError_t launch_ring_p3_f32(bool alpha, const StageArgs &a);
 cudaError_t launch_ring_q_f64(int P, bool alpha, const StageArgs &a);   // P = 101 (Q1), 102 (Q2)
+// the ring kernel with the transposed operator L^T (adjoint moments; fp64 P1/P2)
+cudaError_t launch_ring_adj_f64(int P, bool alpha, const StageArgs &a);
 cudaError_t launch_ring_q_f32(int P, bool alpha, const StageArgs &a);
 
 }  // namespace dgl

@@ -259,7 +259,8 @@ __device__ __forceinline__ void colmv2(T (&accA)[D2][NV], T (&accB)[D2][NV], con
   }
 }
 
-template <typename T, int NV, int P, bool HAS_ALPHA>
+// TR: apply the transposed operator L^T (adjoint moments; P1/P2, REFLECT)
+template <typename T, int NV, int P, bool HAS_ALPHA, bool TR = false>
 __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
     k_stage_ring(const T *__restrict__ Uin, const T *U0, T *Uout, const int4 *__restrict__ nbr,
                  const int4 *__restrict__ rowtab, int nact, int ny, int nstrips, int ngroups, int band_rows,
@@ -653,21 +654,21 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
         // then the fixed neighbour blocks of the open faces
         // (P3: 400-entry blocks; a 16-variant switch would not fit the
         // instruction cache, so the self block is applied as V + sum F_f)
-        if constexpr (P <= 2) mv_self<T, NV, P>(open_code(nb), acc, xs);
+        if constexpr (P <= 2) mv_self<T, NV, P, TR>(open_code(nb), acc, xs);
         else mv_imm<T, NV, P, 0>(acc, xs);
         if (nb.x >= 0) {
           if constexpr (P == 3) mv_imm<T, NV, P, 1>(acc, xs);
           const T *pn = tile1(mc, nb.x);
 #pragma unroll
           for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
-          mv_imm<T, NV, P, 5>(acc, xn);
+          mv_imm<T, NV, P, 5, TR>(acc, xn);
         }
         if (nb.y >= 0) {
           if constexpr (P == 3) mv_imm<T, NV, P, 2>(acc, xs);
           const T *pn = tile1(mc, nb.y);
 #pragma unroll
           for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
-          mv_imm<T, NV, P, 6>(acc, xn);
+          mv_imm<T, NV, P, 6, TR>(acc, xn);
         }
         if (nb.z >= 0) {
           if constexpr (P == 3) mv_imm<T, NV, P, 3>(acc, xs);
@@ -675,7 +676,7 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
           const T *pn = tile1(mn, nb.z);
 #pragma unroll
           for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
-          mv_imm<T, NV, P, 7>(acc, xn);
+          mv_imm<T, NV, P, 7, TR>(acc, xn);
         }
         if (nb.w >= 0) {
           if constexpr (P == 3) mv_imm<T, NV, P, 4>(acc, xs);
@@ -683,7 +684,7 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
           const T *pn = tile1(ms, nb.w);
 #pragma unroll
           for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
-          mv_imm<T, NV, P, 8>(acc, xn);
+          mv_imm<T, NV, P, 8, TR>(acc, xn);
         }
       } else {
         // boundary pixel with absorbing outer faces: blocks of (code, outer)
@@ -822,7 +823,7 @@ inline int alpha_max_ahead(const dgl::StageArgs &a, bool alpha) {
   return alpha ? (a.ahead_alpha > 0 ? a.ahead_alpha : RING_Q - 1) : (a.ahead_noalpha > 0 ? a.ahead_noalpha : RING_Q - 1);
 }
 
-template <typename T, int NV, int P, bool ALPHA>
+template <typename T, int NV, int P, bool ALPHA, bool TR = false>
 cudaError_t launch_ring(const dgl::StageArgs &a) {
   using Gm = RingGeom<T, NV, P, ALPHA>;
   // the dynamic shared-memory opt-in is per device: one bit per ordinal
@@ -835,7 +836,7 @@ cudaError_t launch_ring(const dgl::StageArgs &a) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
   if (!(attr_set.load() >> dev & 1)) {
-    cudaError_t e = cudaFuncSetAttribute(k_stage_ring<T, NV, P, ALPHA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_stage_ring<T, NV, P, ALPHA, TR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Gm::SMEM + pad);
     if (e != cudaSuccess) return e;
     attr_set.fetch_or(uint64_t(1) << dev);
@@ -854,7 +855,7 @@ cudaError_t launch_ring(const dgl::StageArgs &a) {
   nbands = (a.ny + band_rows - 1) / band_rows;
   const int nitems = per_band * nbands;
   const int grid = std::min(nitems, a.nsm);
-  k_stage_ring<T, NV, P, ALPHA><<<grid, Gm::THREADS, Gm::SMEM + pad, a.st>>>(
+  k_stage_ring<T, NV, P, ALPHA, TR><<<grid, Gm::THREADS, Gm::SMEM + pad, a.st>>>(
       (const T *)a.Uin, (const T *)a.U0, (T *)a.Uout, a.nbr, ALPHA ? a.rowtab : a.rowtab_na, a.nact, a.ny,
       ALPHA ? a.nstrips : a.nstrips_na, a.ngroups,
       band_rows, nitems, (T)a.alpha, (T)a.cs, a.diag,

@@ -1092,20 +1092,22 @@ def test_logical_ranks_more_ranks_than_sources(dg, cfg, windows):
     assert np.array_equal(SR, S1) and np.array_equal(muR, mu1)
 
 
-@pytest.mark.parametrize("p", [1, 2])
-def test_adjoint_moments_vs_oracle_and_forward(dg, orc, cfg, p):
+@pytest.mark.parametrize("p,kernel", [(1, 0), (2, 0), (1, 1), (2, 1)])
+def test_adjoint_moments_vs_oracle_and_forward(dg, orc, cfg, p, kernel):
     """opts.adjoint = 1 (round 2): every source's moments from ONE group of
     weight fields stepped with the transposed operator (m_s = (P(dt L^T)^N
-    w_s)^T u0_s).  Against O1 on c1 and a random walled mask (all sources),
-    and against the per-source GPU solve on the c3 substrate (128 sources):
-    per-source moments and Sigma within the fp64 tolerances."""
+    w_s)^T u0_s), on the ring kernel with transposed tables and the sources'
+    domain of dependence (kernel 0) or the v1 table kernel (kernel 1).
+    Against O1 on c1 and a random walled mask (all sources), and against the
+    per-source GPU solve on the c3 substrate (128 sources): per-source moments
+    and Sigma within the fp64 tolerances."""
     t = TOL[64]
     m = cfg.mask("c1")
     src = cfg.sources("c1")
     c = cfg.CONFIGS["c1"]
     dt = c.dt if p == 1 else 1 / 128
     ref = orc.solve(p, 1.0, 1.0, m, src, dt, c.nsteps)
-    with dg.Solver(m, 1.0, 1.0, p, adjoint=1) as s:
+    with dg.Solver(m, 1.0, 1.0, p, adjoint=1, kernel=kernel) as s:
         s.solve(src, dt, c.nsteps)
         S, mu = s.covariance()
         mom = s.moments()
@@ -1116,7 +1118,7 @@ def test_adjoint_moments_vs_oracle_and_forward(dg, orc, cfg, p):
     pick = free[rng.integers(0, len(free), 70)]
     srcs = np.stack([pick[:, 1], pick[:, 0]], 1).astype(np.int32)
     ref = orc.solve(p, 0.8, 1.3, mk, srcs, dt * 0.64 / 1.3, 60)
-    with dg.Solver(mk, 0.8, 1.3, p, adjoint=1) as s:
+    with dg.Solver(mk, 0.8, 1.3, p, adjoint=1, kernel=kernel) as s:
         s.solve(srcs, dt * 0.64 / 1.3, 60)
         S, mu = s.covariance()
         mom = s.moments()
@@ -1129,7 +1131,7 @@ def test_adjoint_moments_vs_oracle_and_forward(dg, orc, cfg, p):
         s.solve(src3, dt, 100)
         S0, _ = s.covariance()
         M0 = s.moments()
-    with dg.Solver(m3, 1.0, 1.0, p, adjoint=1) as s:
+    with dg.Solver(m3, 1.0, 1.0, p, adjoint=1, kernel=kernel) as s:
         s.solve(src3, dt, 100)
         S1, _ = s.covariance()
         M1 = s.moments()
