@@ -275,9 +275,10 @@ def measure_adjoint(args, dg, mask, all_src, dt, nsteps, stream, rank, world, lo
         ms = e0.elapsed_time(e1)
         return {"sources": int(len(all_src)), "nsteps": nsteps, "ms": ms, "sigma_solves_per_s": 1e3 / ms,
                 "sigma": [S[0, 0], S[0, 1], S[1, 1]],
-                "note": "moments of every source from 3 source groups of weight fields stepped with the "
-                        "transposed operator (v1 table kernel) and read at each source pixel; the same Sigma as "
-                        "the per-source solves of the whole job up to rounding (DESIGN 9b, N5)"}
+                "note": "moments of every source from a few source groups of weight fields stepped with the "
+                        "transposed operator (ring kernel, the sources' domain of dependence) and read at each "
+                        "source pixel; the same Sigma as the per-source solves of the whole job up to rounding "
+                        "(DESIGN 9b, N5)"}
     finally:
         s.close()
 

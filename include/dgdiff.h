@@ -140,11 +140,13 @@ typedef struct {
                              six weight fields of 1, x, y, x^2, xy, y^2 about a
                              nearby origin; so dgdiff_solve_batch evolves those
                              fields (30 origins on a lattice over the sources'
-                             box: 180 lanes of three 64-lane groups) with the
-                             transposed composite operator (v1 table kernel)
-                             and reads every source's moments from them at its
-                             pixel: three groups of work for any number of
-                             sources.  Same Sigma as the
+                             box: 3 groups of 64 lanes for P1, 6 of 32 for P2)
+                             with the transposed composite operator (ring
+                             kernel with transposed tables over the sources'
+                             domain of dependence; kernel = 1: the v1 table
+                             kernel) and reads every source's moments from
+                             them at its pixel: a few groups of work for any
+                             number of sources.  Same Sigma as the
                              per-source solve up to rounding (the centring
                              subtraction loses ~log10(box^2 / m_20) digits).
                              fp64, P1/P2 triangles, REFLECT, no windows,
