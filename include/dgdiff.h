@@ -149,6 +149,7 @@ typedef struct {
                              number of sources.  Same Sigma as the
                              per-source solve up to rounding (the centring
                              subtraction loses ~log10(box^2 / m_20) digits).
+                             Pixel sources and N4 sub-pixel points.
                              fp64, P1/P2 triangles, REFLECT, no windows,
                              mixture, temporal blocking or densities (E_ARG);
                              0 (default) = per-source forward solves */

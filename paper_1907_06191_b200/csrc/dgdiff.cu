@@ -282,14 +282,16 @@ __global__ void k_adj_init(double *__restrict__ U, const int2 *__restrict__ pix,
 template <int D2, int G>
 __global__ void k_adj_eval(const double *__restrict__ U, int nact, const int32_t *__restrict__ src, int64_t b, int64_t nloc,
                            const int *__restrict__ aidx, int nx, double h, InitVals iv, AdjOrigins org,
-                           double *__restrict__ mom) {
+                           double *__restrict__ mom, const double *__restrict__ px /* nullable: points, shard rows */) {
   constexpr int OPG = adj_per_group<G>();
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= nloc) return;
   const int64_t s = b + k;
   const int i = src[2 * s], j = src[2 * s + 1];
   const int a = __ldg(&aidx[(size_t)j * nx + i]);
-  const double xs = i + 0.5, ys = j + 0.5;
+  // N4 sub-pixel points: the point and its projected-Dirac row (R21)
+  const double *row = px ? px + k * (2 + D2) : nullptr;
+  const double xs = row ? row[0] : i + 0.5, ys = row ? row[1] : j + 0.5;
   int o = 0;
   double best = 1e300;
   for (int c = 0; c < org.n; c++) {
@@ -302,7 +304,8 @@ __global__ void k_adj_eval(const double *__restrict__ U, int nact, const int32_t
     double e = 0.0;
 #pragma unroll
     for (int kk = 0; kk < D2; kk++)
-      e = fma(U[(size_t)(o / OPG) * nact * D2 * G + ((size_t)a * D2 + kk) * G + 6 * (o % OPG) + q], iv.v[kk], e);
+      e = fma(U[(size_t)(o / OPG) * nact * D2 * G + ((size_t)a * D2 + kk) * G + 6 * (o % OPG) + q],
+              row ? row[2 + kk] : iv.v[kk], e);
     E[q] = e;
   }
   const double dX = h * (xs - org.x[o]), dY = h * (ys - org.y[o]);
@@ -1524,8 +1527,8 @@ static dgdiff_status run_chunk_p(dgdiff_s *H, int64_t nvalid, int64_t chunk, dou
 // transposed table (opts.kernel = 1) -- then every source of the shard
 // [b, b + nloc) is evaluated into its table row.
 template <int D2, int G>
-static dgdiff_status adjoint_solve(dgdiff_s *H, const int32_t *sources, int64_t b, int64_t nloc, double dt,
-                                   int64_t nsteps) {
+static dgdiff_status adjoint_solve(dgdiff_s *H, const int32_t *sources, const double *px, int64_t b, int64_t nloc,
+                                   double dt, int64_t nsteps) {
   constexpr int NG = adj_groups<G>();
   const int P = D2 == 6 ? 1 : 2;
   const int nact = (int)H->nact;
@@ -1632,8 +1635,21 @@ static dgdiff_status adjoint_solve(dgdiff_s *H, const int32_t *sources, int64_t 
     InitVals iv;
     const double ih2 = 1.0 / (H->h * H->h);
     for (int k = 0; k < D2; k++) iv.v[k] = H->tab.init[k] * ih2;
+    const double *dpx = nullptr;
+    if (px) {   // N4 points: this shard's rows (point + projected-Dirac row)
+      const size_t PXS = 2 + D2;
+      if (nloc > H->px_cap) {
+        cudaFree(H->d_px);
+        H->d_px = nullptr;
+        CK(cudaMalloc(&H->d_px, sizeof(double) * PXS * nloc));
+        H->px_cap = nloc;
+      }
+      CK(cudaMemcpyAsync(H->d_px, px + (size_t)b * PXS, sizeof(double) * PXS * nloc, cudaMemcpyHostToDevice, st));
+      H->st.h2d_bytes += sizeof(double) * PXS * nloc;
+      dpx = H->d_px;
+    }
     k_adj_eval<D2, G><<<(int)((nloc + 127) / 128), 128, 0, st>>>(u, nact, H->d_src, b, nloc, H->d_aidx, H->nx, H->h,
-                                                                 iv, org, H->d_mom);
+                                                                 iv, org, H->d_mom, dpx);
     H->st.launches++;
   }
   CK(cudaGetLastError());
@@ -1704,12 +1720,11 @@ static dgdiff_status solve_impl(dgdiff_s *H, const int32_t *sources, const doubl
   CK(cudaMemcpyAsync(H->d_src, H->h_src_stage.data(), sizeof(int32_t) * 2 * n, cudaMemcpyHostToDevice, H->stream));
   H->st.h2d_bytes += sizeof(int32_t) * 2 * n;
   if (H->o.adjoint) {
-    if (px) return fail(DGDIFF_E_ARG, "adjoint moments: pixel sources only");
     const int G = gsize(H);
-    dgdiff_status r = H->D2 == 6 ? (G == 64 ? adjoint_solve<6, 64>(H, sources, b, nloc, dt, nsteps)
-                                            : adjoint_solve<6, 32>(H, sources, b, nloc, dt, nsteps))
-                                 : (G == 64 ? adjoint_solve<12, 64>(H, sources, b, nloc, dt, nsteps)
-                                            : adjoint_solve<12, 32>(H, sources, b, nloc, dt, nsteps));
+    dgdiff_status r = H->D2 == 6 ? (G == 64 ? adjoint_solve<6, 64>(H, sources, px, b, nloc, dt, nsteps)
+                                            : adjoint_solve<6, 32>(H, sources, px, b, nloc, dt, nsteps))
+                                 : (G == 64 ? adjoint_solve<12, 64>(H, sources, px, b, nloc, dt, nsteps)
+                                            : adjoint_solve<12, 32>(H, sources, px, b, nloc, dt, nsteps));
     if (r != DGDIFF_OK) return r;
     H->solved = true;
     H->last_n = n;

@@ -1137,3 +1137,31 @@ def test_adjoint_moments_vs_oracle_and_forward(dg, orc, cfg, p, kernel):
         M1 = s.moments()
     assert mom_err(M1, M0) <= t["mom"]
     assert sig_err(S1, S0) <= t["sig"]
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_adjoint_moments_subpixel_points_vs_oracle(dg, orc, p):
+    """opts.adjoint with N4 sub-pixel point sources (R21): each point's
+    moments are its evolved weight fields read against the point's
+    projected-Dirac row, re-centred on the point; against O1's
+    solve_points."""
+    rng = np.random.default_rng(610 + p)
+    ny, nx = 26, 30
+    m = (rng.random((ny, nx)) < 0.3).astype(np.uint8)
+    free = np.argwhere(m == 0)
+    pick = free[rng.integers(0, len(free), 40)]
+    loc = rng.random((40, 2))
+    loc[0] = (0.3, 0.3)
+    loc[1] = (0.0, 0.6)
+    h = 0.8
+    pts = (np.stack([pick[:, 1], pick[:, 0]], 1) + loc) * h
+    dt = (1 / 32 if p == 1 else 1 / 128) * h * h
+    ref = orc.solve_points(p, h, 1.0, m, pts, dt, 40)
+    with dg.Solver(m, h, 1.0, p, adjoint=1) as s:
+        s.solve_points(pts, dt, 40)
+        S, mu = s.covariance()
+        mom = s.moments()
+    t = TOL[64]
+    assert mom_err(mom, ref) <= t["mom"]
+    R, _ = orc.sigma(ref)
+    assert sig_err(S, R) <= t["sig"]
