@@ -1515,7 +1515,7 @@ static dgdiff_status run_chunk_p(dgdiff_s *H, int64_t nvalid, int64_t chunk, dou
 }
 
 // Adjoint moments (opts.adjoint): see k_adj_init.  The weight fields of up to
-// 30 origins (a lattice over the box of this rank's sources, so that
+// 30 origins (a lattice over the box of the batch's sources, so that
 // |x_s - x_o| stays small and the re-centring subtraction loses few digits:
 // with 9 origins the worst c4 source's second moments differed from the
 // per-source solve by 1.4e-10) fill ceil(30 / (G / 6)) source groups; they
@@ -1527,8 +1527,8 @@ static dgdiff_status run_chunk_p(dgdiff_s *H, int64_t nvalid, int64_t chunk, dou
 // transposed table (opts.kernel = 1) -- then every source of the shard
 // [b, b + nloc) is evaluated into its table row.
 template <int D2, int G>
-static dgdiff_status adjoint_solve(dgdiff_s *H, const int32_t *sources, const double *px, int64_t b, int64_t nloc,
-                                   double dt, int64_t nsteps) {
+static dgdiff_status adjoint_solve(dgdiff_s *H, const int32_t *sources, const double *px, int64_t n, int64_t b,
+                                   int64_t nloc, double dt, int64_t nsteps) {
   constexpr int NG = adj_groups<G>();
   const int P = D2 == 6 ? 1 : 2;
   const int nact = (int)H->nact;
@@ -1547,12 +1547,14 @@ static dgdiff_status adjoint_solve(dgdiff_s *H, const int32_t *sources, const do
   org.n = 0;
   int4 box = make_int4(0, H->nx - 1, 0, H->ny - 1);
   if (nloc > 0) {
+    // the origin lattice spans the WHOLE batch (every rank sees the same
+    // list), so a source's moments do not depend on the rank count
     int x0 = INT32_MAX, x1 = INT32_MIN, y0 = INT32_MAX, y1 = INT32_MIN;
-    for (int64_t k = 0; k < nloc; k++) {
-      x0 = std::min(x0, sources[2 * (b + k)]);
-      x1 = std::max(x1, sources[2 * (b + k)]);
-      y0 = std::min(y0, sources[2 * (b + k) + 1]);
-      y1 = std::max(y1, sources[2 * (b + k) + 1]);
+    for (int64_t k = 0; k < n; k++) {
+      x0 = std::min(x0, sources[2 * k]);
+      x1 = std::max(x1, sources[2 * k]);
+      y0 = std::min(y0, sources[2 * k + 1]);
+      y1 = std::max(y1, sources[2 * k + 1]);
     }
     box = make_int4(x0, x1, y0, y1);
     // a kx x ky lattice of cell centres (kx ky <= ADJ_MAXO), cells as square
@@ -1721,10 +1723,10 @@ static dgdiff_status solve_impl(dgdiff_s *H, const int32_t *sources, const doubl
   H->st.h2d_bytes += sizeof(int32_t) * 2 * n;
   if (H->o.adjoint) {
     const int G = gsize(H);
-    dgdiff_status r = H->D2 == 6 ? (G == 64 ? adjoint_solve<6, 64>(H, sources, px, b, nloc, dt, nsteps)
-                                            : adjoint_solve<6, 32>(H, sources, px, b, nloc, dt, nsteps))
-                                 : (G == 64 ? adjoint_solve<12, 64>(H, sources, px, b, nloc, dt, nsteps)
-                                            : adjoint_solve<12, 32>(H, sources, px, b, nloc, dt, nsteps));
+    dgdiff_status r = H->D2 == 6 ? (G == 64 ? adjoint_solve<6, 64>(H, sources, px, n, b, nloc, dt, nsteps)
+                                            : adjoint_solve<6, 32>(H, sources, px, n, b, nloc, dt, nsteps))
+                                 : (G == 64 ? adjoint_solve<12, 64>(H, sources, px, n, b, nloc, dt, nsteps)
+                                            : adjoint_solve<12, 32>(H, sources, px, n, b, nloc, dt, nsteps));
     if (r != DGDIFF_OK) return r;
     H->solved = true;
     H->last_n = n;

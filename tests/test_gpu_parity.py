@@ -1165,3 +1165,24 @@ def test_adjoint_moments_subpixel_points_vs_oracle(dg, orc, p):
     assert mom_err(mom, ref) <= t["mom"]
     R, _ = orc.sigma(ref)
     assert sig_err(S, R) <= t["sig"]
+
+
+def test_adjoint_logical_ranks_bitwise(dg, cfg):
+    """Adjoint moments under logical ranks: the origin lattice spans the whole
+    batch, so the summed R-rank tables and Sigma equal one rank bit for bit."""
+    m = cfg.mask("c3")
+    src = cfg.sources("c3")[:300]
+    with dg.Solver(m, 1.0, 1.0, 1, adjoint=1) as s:
+        s.solve(src, 1 / 32, 24)
+        S1, mu1 = s.covariance()
+        M1 = s.moments()
+    for R in (2, 4):
+        tab = np.zeros_like(M1)
+        for r in range(R):
+            with dg.Solver(m, 1.0, 1.0, 1, adjoint=1, rank=r, nranks=R) as s:
+                s.solve(src, 1 / 32, 24)
+                tab += s.moments()
+                if r == R - 1:
+                    SR, muR = s.covariance_table(tab)
+        assert np.array_equal(tab, M1), R
+        assert np.array_equal(SR, S1) and np.array_equal(muR, mu1), R
