@@ -1534,6 +1534,7 @@ static dgdiff_status adjoint_solve(dgdiff_s *H, const int32_t *sources, const do
   const int nact = (int)H->nact;
   const bool ring = use_ring(H);
   cudaStream_t st = H->stream;
+  if (nloc == 0) return DGDIFF_OK;   // an empty shard: its table rows stay zero
   if (H->chunk_cap < NG * G) {
     cudaFree(H->d_Ubase);
     H->d_Ubase = nullptr;
