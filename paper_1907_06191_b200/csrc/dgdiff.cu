@@ -1150,11 +1150,11 @@ extern "C" dgdiff_status dgdiff_create(dgdiff_t *out, const uint8_t *mask, int32
   if (o.max_chunk < 0) return fail(DGDIFF_E_ARG, "max_chunk < 0");
   if (o.mixture_radius < 0 || o.mixture_radius > 2048) return fail(DGDIFF_E_ARG, "mixture_radius must be in [0, 2048]");
   if (o.adjoint != 0 && o.adjoint != 1) return fail(DGDIFF_E_ARG, "adjoint must be 0 or 1");
-  if (o.adjoint == 1 && (o.precision != 64 || degree > 2 || o.element != 0 || o.outer_bc != 0 || o.windows != 0 ||
+  if (o.adjoint == 1 && (degree > 2 || o.element != 0 || o.outer_bc != 0 || o.windows != 0 ||
                          o.temporal_steps > 1 || o.kernel == 2 || o.kernel == 3 || o.mixture_radius != 0 ||
-                         o.keep_density != 0))
-    return fail(DGDIFF_E_ARG, "adjoint moments: fp64 P1/P2 triangles, REFLECT, no windows / temporal blocking / "
-                              "mixture / densities");
+                         o.keep_density != 0 || (o.precision == 32 && o.kernel == 1)))
+    return fail(DGDIFF_E_ARG, "adjoint moments: P1/P2 triangles, REFLECT, no windows / temporal blocking / "
+                              "mixture / densities (fp32 handles: ring kernel)");
   dgdiff_s *H = new dgdiff_s();
   H->nx = nx; H->ny = ny; H->h = h; H->D = D; H->p = degree;
   H->d = (degree + 1) * (degree + 2) / 2;
@@ -1723,7 +1723,9 @@ static dgdiff_status solve_impl(dgdiff_s *H, const int32_t *sources, const doubl
   CK(cudaMemcpyAsync(H->d_src, H->h_src_stage.data(), sizeof(int32_t) * 2 * n, cudaMemcpyHostToDevice, H->stream));
   H->st.h2d_bytes += sizeof(int32_t) * 2 * n;
   if (H->o.adjoint) {
-    const int G = gsize(H);
+    // the adjoint fields are fp64 whatever the handle's precision (the
+    // re-centring needs the digits): the fp64 lane width of the kernel used
+    const int G = use_ring(H) ? (H->D2 == 6 ? 64 : 32) : 64;
     dgdiff_status r = H->D2 == 6 ? (G == 64 ? adjoint_solve<6, 64>(H, sources, px, n, b, nloc, dt, nsteps)
                                             : adjoint_solve<6, 32>(H, sources, px, n, b, nloc, dt, nsteps))
                                  : (G == 64 ? adjoint_solve<12, 64>(H, sources, px, n, b, nloc, dt, nsteps)

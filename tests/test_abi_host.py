@@ -229,9 +229,9 @@ def test_argument_errors_are_reported(dg):
         with pytest.raises(dg.DGDiffError) as e:
             dg.dgdiff_create(np.zeros((4, 4), np.uint8), 1.0, 1.0, 1, dg.dgdiff_opts_default(**bad))
         assert e.value.status == dg.E_ARG, bad
-    # adjoint moments: fp64 P1/P2 triangles, REFLECT, none of windows /
-    # temporal blocking / mixture / densities
-    for bad in (dict(adjoint=2), dict(adjoint=1, precision=32), dict(adjoint=1, element=1),
+    # adjoint moments: P1/P2 triangles, REFLECT, none of windows / temporal
+    # blocking / mixture / densities; fp32 handles on the ring kernel only
+    for bad in (dict(adjoint=2), dict(adjoint=1, precision=32, kernel=1), dict(adjoint=1, element=1),
                 dict(adjoint=1, outer_bc=1), dict(adjoint=1, windows=1), dict(adjoint=1, temporal_steps=5),
                 dict(adjoint=1, mixture_radius=3), dict(adjoint=1, keep_density=1), dict(adjoint=1, kernel=3)):
         with pytest.raises(dg.DGDiffError) as e:

@@ -1186,3 +1186,22 @@ def test_adjoint_logical_ranks_bitwise(dg, cfg):
                     SR, muR = s.covariance_table(tab)
         assert np.array_equal(tab, M1), R
         assert np.array_equal(SR, S1) and np.array_equal(muR, mu1), R
+
+
+def test_adjoint_on_fp32_handle_is_fp64_accurate(dg, orc, cfg):
+    """An fp32 handle with adjoint = 1 steps the (fp64) weight fields: its
+    moments meet the fp64 tolerance against O1, not only the fp32 one."""
+    rng = np.random.default_rng(77)
+    mk = (rng.random((28, 31)) < 0.35).astype(np.uint8)
+    free = np.argwhere(mk == 0)
+    pick = free[rng.integers(0, len(free), 50)]
+    srcs = np.stack([pick[:, 1], pick[:, 0]], 1).astype(np.int32)
+    for p, dt in ((1, 1 / 32), (2, 1 / 128)):
+        ref = orc.solve(p, 1.0, 1.0, mk, srcs, dt, 50)
+        with dg.Solver(mk, 1.0, 1.0, p, precision=32, adjoint=1) as s:
+            s.solve(srcs, dt, 50)
+            S, mu = s.covariance()
+            mom = s.moments()
+        assert mom_err(mom, ref) <= TOL[64]["mom"], p
+        R, _ = orc.sigma(ref)
+        assert sig_err(S, R) <= TOL[64]["sig"], p
