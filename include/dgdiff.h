@@ -151,8 +151,9 @@ typedef struct {
                              subtraction loses ~log10(box^2 / m_20) digits).
                              Pixel sources and N4 sub-pixel points.  The
                              fields are fp64 also on fp32 handles (ring kernel).
-                             P1/P2 triangles, REFLECT, no windows,
-                             mixture, temporal blocking or densities (E_ARG);
+                             P1/P2 triangles or Q1/Q2 (ring kernel), REFLECT,
+                             no windows, mixture, temporal blocking or
+                             densities (E_ARG);
                              0 (default) = per-source forward solves */
 } dgdiff_opts;
 

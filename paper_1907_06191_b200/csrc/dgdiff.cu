@@ -246,10 +246,10 @@ template <int G> __host__ __device__ constexpr int adj_per_group() { return G / 
 template <int G> __host__ __device__ constexpr int adj_groups() { return (ADJ_MAXO + G / 6 - 1) / (G / 6); }
 struct AdjOrigins { double x[ADJ_MAXO], y[ADJ_MAXO]; int n; };
 
-template <int D2, int G>
+template <int D2, int G, int NT>
 __global__ void k_adj_init(double *__restrict__ U, const int2 *__restrict__ pix, int nact, double h, MomW mw,
                            AdjOrigins org) {
-  constexpr int d = D2 / 2, OPG = adj_per_group<G>();
+  constexpr int d = D2 / NT, OPG = adj_per_group<G>();   // NT elements per pixel (quads: 1)
   const int64_t per_group = (int64_t)nact * D2 * G;
   const int64_t total = per_group * adj_groups<G>();
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
@@ -1150,11 +1150,11 @@ extern "C" dgdiff_status dgdiff_create(dgdiff_t *out, const uint8_t *mask, int32
   if (o.max_chunk < 0) return fail(DGDIFF_E_ARG, "max_chunk < 0");
   if (o.mixture_radius < 0 || o.mixture_radius > 2048) return fail(DGDIFF_E_ARG, "mixture_radius must be in [0, 2048]");
   if (o.adjoint != 0 && o.adjoint != 1) return fail(DGDIFF_E_ARG, "adjoint must be 0 or 1");
-  if (o.adjoint == 1 && (degree > 2 || o.element != 0 || o.outer_bc != 0 || o.windows != 0 ||
-                         o.temporal_steps > 1 || o.kernel == 2 || o.kernel == 3 || o.mixture_radius != 0 ||
-                         o.keep_density != 0 || (o.precision == 32 && o.kernel == 1)))
-    return fail(DGDIFF_E_ARG, "adjoint moments: P1/P2 triangles, REFLECT, no windows / temporal blocking / "
-                              "mixture / densities (fp32 handles: ring kernel)");
+  if (o.adjoint == 1 && (degree > 2 || o.outer_bc != 0 || o.windows != 0 || o.temporal_steps > 1 || o.kernel == 2 ||
+                         o.kernel == 3 || o.mixture_radius != 0 || o.keep_density != 0 ||
+                         ((o.precision == 32 || o.element == 1) && o.kernel == 1)))
+    return fail(DGDIFF_E_ARG, "adjoint moments: P1/P2 triangles or Q1/Q2, REFLECT, no windows / temporal blocking / "
+                              "mixture / densities (fp32 handles and quads: ring kernel)");
   dgdiff_s *H = new dgdiff_s();
   H->nx = nx; H->ny = ny; H->h = h; H->D = D; H->p = degree;
   H->d = (degree + 1) * (degree + 2) / 2;
@@ -1526,11 +1526,11 @@ static dgdiff_status run_chunk_p(dgdiff_s *H, int64_t nvalid, int64_t chunk, dou
 // keep stale values that are never read), or on the v1 table kernel with the
 // transposed table (opts.kernel = 1) -- then every source of the shard
 // [b, b + nloc) is evaluated into its table row.
-template <int D2, int G>
+template <int D2, int G, int NT = 2>
 static dgdiff_status adjoint_solve(dgdiff_s *H, const int32_t *sources, const double *px, int64_t n, int64_t b,
                                    int64_t nloc, double dt, int64_t nsteps) {
   constexpr int NG = adj_groups<G>();
-  const int P = D2 == 6 ? 1 : 2;
+  const int P = NT == 1 ? (D2 == 4 ? 101 : 102) : (D2 == 6 ? 1 : 2);
   const int nact = (int)H->nact;
   const bool ring = use_ring(H);
   cudaStream_t st = H->stream;
@@ -1576,7 +1576,7 @@ static dgdiff_status adjoint_solve(dgdiff_s *H, const int32_t *sources, const do
   }
   double *u = (double *)H->d_U[0], *Ua = (double *)H->d_U[1], *Ub = (double *)H->d_U[2];
   const int64_t total = (int64_t)nact * D2 * G * NG;
-  k_adj_init<D2, G><<<(int)std::min<int64_t>((total + 255) / 256, 148 * 64), 256, 0, st>>>(u, H->d_pix, nact, H->h,
+  k_adj_init<D2, G, NT><<<(int)std::min<int64_t>((total + 255) / 256, 148 * 64), 256, 0, st>>>(u, H->d_pix, nact, H->h,
                                                                                               H->momw, org);
   H->st.launches++;
   dgl::StageArgs sa;
@@ -1597,6 +1597,10 @@ static dgdiff_status adjoint_solve(dgdiff_s *H, const int32_t *sources, const do
     sa.n1_use = H->n1_use;
     sa.n1_use_na = H->n1_use > 0 ? H->n1_use : (int)(8.0 * H->mean_tile + 0.5);
     sa.n2_use = H->n2_use;
+    sa.nbi = H->d_nbi[1];   // quads: item neighbour buffers
+    sa.nbi_off = H->d_nbi_off[1];
+    sa.nbi_na = H->d_nbi[0];
+    sa.nbi_off_na = H->d_nbi_off[0];
     // every group clips to the sources' box grown by the remaining reach
     std::vector<int4> gb(NG, box);
     if (NG > H->gbox_cap) {
@@ -1726,7 +1730,9 @@ static dgdiff_status solve_impl(dgdiff_s *H, const int32_t *sources, const doubl
     // the adjoint fields are fp64 whatever the handle's precision (the
     // re-centring needs the digits): the fp64 lane width of the kernel used
     const int G = use_ring(H) ? (H->D2 == 6 ? 64 : 32) : 64;
-    dgdiff_status r = H->D2 == 6 ? (G == 64 ? adjoint_solve<6, 64>(H, sources, px, n, b, nloc, dt, nsteps)
+    dgdiff_status r = H->quad ? (H->D2 == 4 ? adjoint_solve<4, 32, 1>(H, sources, px, n, b, nloc, dt, nsteps)
+                                            : adjoint_solve<9, 32, 1>(H, sources, px, n, b, nloc, dt, nsteps))
+                    : H->D2 == 6 ? (G == 64 ? adjoint_solve<6, 64>(H, sources, px, n, b, nloc, dt, nsteps)
                                             : adjoint_solve<6, 32>(H, sources, px, n, b, nloc, dt, nsteps))
                                  : (G == 64 ? adjoint_solve<12, 64>(H, sources, px, n, b, nloc, dt, nsteps)
                                             : adjoint_solve<12, 32>(H, sources, px, n, b, nloc, dt, nsteps));

@@ -165,18 +165,26 @@ static int emit_quad(FILE *f, int p) {
   dgop::QuadTable T = dgop::build_quad(p);
   const int d = T.d;
   fprintf(f, "// Q%d: 28 blocks of %dx%d (0-15 self[code], 16+f N_f opp. open, 20+f N_f opp. closed, 24+f NN_f)\n", p, d, d);
-  fprintf(f, "__host__ __device__ constexpr double tab_q%d(int b, int r, int c) {\n  switch ((b * %d + r) * %d + c) {\n", p, d, d);
-  int nnz = 0;
-  for (int b = 0; b < 28; b++)
-    for (int r = 0; r < d; r++)
-      for (int c = 0; c < d; c++) {
-        const double v = T.blocks[((size_t)b * d + r) * d + c];
-        if (v != 0.0) {
-          fprintf(f, "    case %d: return %a;\n", (b * d + r) * d + c, v);
-          nnz++;
+  // tr = 1: the transposed operator L^T (adjoint moments): self blocks
+  // transposed; the blocks of face f and of the far pixel in direction f are
+  // the transposed blocks of the OPPOSITE direction (variant ids kept: the
+  // kernel picks the face variant by the far pixel's state under L^T)
+  for (int tr = 0; tr < 2; tr++) {
+    fprintf(f, "__host__ __device__ constexpr double tab_q%d%s(int b, int r, int c) {\n  switch ((b * %d + r) * %d + c) {\n",
+            p, tr ? "t" : "", d, d);
+    int nnz = 0;
+    for (int b = 0; b < 28; b++)
+      for (int r = 0; r < d; r++)
+        for (int c = 0; c < d; c++) {
+          const int bs = (tr && b >= 16) ? 16 + ((b - 16) / 4) * 4 + (((b - 16) % 4) ^ 1) : b;   // E<->W, N<->S
+          const double v = tr ? T.blocks[((size_t)bs * d + c) * d + r] : T.blocks[((size_t)b * d + r) * d + c];
+          if (v != 0.0) {
+            fprintf(f, "    case %d: return %a;\n", (b * d + r) * d + c, v);
+            nnz++;
+          }
         }
-      }
-  fprintf(f, "    default: return 0.0;\n  }\n}\n// nnz(Q%d) = %d\n\n", p, nnz);
+    fprintf(f, "    default: return 0.0;\n  }\n}\n// nnz(Q%d%s) = %d\n\n", p, tr ? "t" : "", nnz);
+  }
   return 0;
 }
 

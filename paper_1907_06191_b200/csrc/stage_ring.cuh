@@ -572,53 +572,55 @@ __global__ void __launch_bounds__(RingGeom<T, NV, P, HAS_ALPHA>::THREADS, 1)
             }
           }
         } else {
-        mv_self<T, NV, P>(code, acc, xs);
+        // (TR, the transposed operator: the face-f block's variant follows the
+        // state of the pixel two steps on, whose face decides L's block there)
+        mv_self<T, NV, P, TR>(code, acc, xs);
         if (nb.x >= 0) {
           const T *pn = tile1(mc, nb.x);
 #pragma unroll
           for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
-          if (nb.y >= 0) mv_imm<T, NV, P, 16>(acc, xn); else mv_imm<T, NV, P, 20>(acc, xn);
+          if (TR ? nb2.x >= 0 : nb.y >= 0) mv_imm<T, NV, P, 16, TR>(acc, xn); else mv_imm<T, NV, P, 20, TR>(acc, xn);
           if (nb2.x >= 0) {
             const T *pf = tile1(mc, nb2.x);
 #pragma unroll
             for (int k = 0; k < D2; k++) lds<T, NV>(pf + k * G, xn[k]);
-            mv_imm<T, NV, P, 24>(acc, xn);
+            mv_imm<T, NV, P, 24, TR>(acc, xn);
           }
         }
         if (nb.y >= 0) {
           const T *pn = tile1(mc, nb.y);
 #pragma unroll
           for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
-          if (nb.x >= 0) mv_imm<T, NV, P, 17>(acc, xn); else mv_imm<T, NV, P, 21>(acc, xn);
+          if (TR ? nb2.y >= 0 : nb.x >= 0) mv_imm<T, NV, P, 17, TR>(acc, xn); else mv_imm<T, NV, P, 21, TR>(acc, xn);
           if (nb2.y >= 0) {
             const T *pf = tile1(mc, nb2.y);
 #pragma unroll
             for (int k = 0; k < D2; k++) lds<T, NV>(pf + k * G, xn[k]);
-            mv_imm<T, NV, P, 25>(acc, xn);
+            mv_imm<T, NV, P, 25, TR>(acc, xn);
           }
         }
         if (nb.z >= 0) {
           const T *pn = tile1(meta[seq(j + 1) % Q], nb.z);
 #pragma unroll
           for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
-          if (nb.w >= 0) mv_imm<T, NV, P, 18>(acc, xn); else mv_imm<T, NV, P, 22>(acc, xn);
+          if (TR ? nb2.z >= 0 : nb.w >= 0) mv_imm<T, NV, P, 18, TR>(acc, xn); else mv_imm<T, NV, P, 22, TR>(acc, xn);
           if (nb2.z >= 0) {
             const T *pf = tile1(meta[seq(j + 2) % Q], nb2.z);
 #pragma unroll
             for (int k = 0; k < D2; k++) lds<T, NV>(pf + k * G, xn[k]);
-            mv_imm<T, NV, P, 26>(acc, xn);
+            mv_imm<T, NV, P, 26, TR>(acc, xn);
           }
         }
         if (nb.w >= 0) {
           const T *pn = tile1(meta[seq(j - 1) % Q], nb.w);
 #pragma unroll
           for (int k = 0; k < D2; k++) lds<T, NV>(pn + k * G, xn[k]);
-          if (nb.z >= 0) mv_imm<T, NV, P, 19>(acc, xn); else mv_imm<T, NV, P, 23>(acc, xn);
+          if (TR ? nb2.w >= 0 : nb.z >= 0) mv_imm<T, NV, P, 19, TR>(acc, xn); else mv_imm<T, NV, P, 23, TR>(acc, xn);
           if (nb2.w >= 0) {
             const T *pf = tile1(meta[seq(j - 2) % Q], nb2.w);
 #pragma unroll
             for (int k = 0; k < D2; k++) lds<T, NV>(pf + k * G, xn[k]);
-            mv_imm<T, NV, P, 27>(acc, xn);
+            mv_imm<T, NV, P, 27, TR>(acc, xn);
           }
         }
         }   // interior / REFLECT quads

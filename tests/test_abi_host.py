@@ -231,7 +231,7 @@ def test_argument_errors_are_reported(dg):
         assert e.value.status == dg.E_ARG, bad
     # adjoint moments: P1/P2 triangles, REFLECT, none of windows / temporal
     # blocking / mixture / densities; fp32 handles on the ring kernel only
-    for bad in (dict(adjoint=2), dict(adjoint=1, precision=32, kernel=1), dict(adjoint=1, element=1),
+    for bad in (dict(adjoint=2), dict(adjoint=1, precision=32, kernel=1), dict(adjoint=1, element=1, kernel=1),
                 dict(adjoint=1, outer_bc=1), dict(adjoint=1, windows=1), dict(adjoint=1, temporal_steps=5),
                 dict(adjoint=1, mixture_radius=3), dict(adjoint=1, keep_density=1), dict(adjoint=1, kernel=3)):
         with pytest.raises(dg.DGDiffError) as e:

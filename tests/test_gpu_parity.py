@@ -1205,3 +1205,26 @@ def test_adjoint_on_fp32_handle_is_fp64_accurate(dg, orc, cfg):
         assert mom_err(mom, ref) <= TOL[64]["mom"], p
         R, _ = orc.sigma(ref)
         assert sig_err(S, R) <= TOL[64]["sig"], p
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_adjoint_moments_quads_vs_oracle(dg, orc, p):
+    """opts.adjoint for N4 quadrilaterals: the transposed 9-point cross (the
+    face block's variant follows the pixel two steps on) on the ring kernel,
+    against O1's quad path on a random walled mask."""
+    rng = np.random.default_rng(820 + p)
+    mk = (rng.random((27, 31)) < 0.35).astype(np.uint8)
+    free = np.argwhere(mk == 0)
+    pick = free[rng.integers(0, len(free), 45)]
+    srcs = np.stack([pick[:, 1], pick[:, 0]], 1).astype(np.int32)
+    h, D = 0.8, 1.4
+    dt = (1 / 16 if p == 1 else 1 / 64) * h * h / D
+    ref = orc.q_solve(p, h, D, mk, srcs, dt, 40)
+    with dg.Solver(mk, h, D, p, element=1, adjoint=1) as s:
+        s.solve(srcs, dt, 40)
+        S, mu = s.covariance()
+        mom = s.moments()
+    t = TOL[64]
+    assert mom_err(mom, ref) <= t["mom"]
+    R, _ = orc.sigma(ref)
+    assert sig_err(S, R) <= t["sig"]
